@@ -1,0 +1,300 @@
+"""Benchmark: Jacobi-PCG iterations/s on the doubly augmented KKT system.
+
+Workload (BASELINE.json configs[4], "cfg5"): the isolated PCG operator sweep
+-- random CSR A 4,000,000 x 1,000,000 with 16 nnz/row (fp64), H =
+diag(U(1e-2,1)), W with log10 w ~ U(-6,6), a fixed 500 Jacobi-PCG iterations
+from a random right-hand side (x0 = 0).  It is the configuration the metric
+"PCG iterations/s and achieved HBM GB/s" is quoted on and the largest one whose
+headline is the PCG sweep; see DESIGN.md section "Measurement".
+
+One step = one direction solve = one call of the hot path: Jacobi build +
+500 PCG iterations + the final true-residual apply (linalg.py:132-133).
+
+  value  PCG iterations/s, whole job, inputs resident in HBM
+         (qpk_pcg_dev on device buffers), CUDA events on the solver's stream
+  e2e    the same metric through the reference-facing drop-in
+         gpu_direction(op, rhs, cfg) with host buffers: diagonals + rhs H2D,
+         Jacobi build, PCG, solution D2H inside the timed region
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Jacobi-PCG iterations/s on the doubly augmented KKT system (cfg5 operator sweep)"
+UNIT = "PCG iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters", type=int, default=500, help="PCG iterations per step (BASELINE cfg5: 500)")
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink cfg5 (testing only; 1.0 = BASELINE)")
+    ap.add_argument("--scatter", type=int, default=1, help="1 = atomic B'z, 2 = CSC gather (deterministic)")
+    ap.add_argument("--cpu-iters", type=int, default=10, help="oracle iterations in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-iters-per-step", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_workload(scale: float, seed: int = 5):
+    from paper_2308_00637_b200 import workloads
+    from paper_2308_00637_b200.problem import build_operator
+    m, n = int(4_000_000 * scale), int(1_000_000 * scale)
+    problem, state, meta = workloads.random_sweep(seed=seed, m=m, n=n)
+    op = build_operator(problem, state)
+    return problem, op, meta
+
+
+def algorithmic_bytes(op, iters: int, applies: int):
+    """bytes_B = 12 nnz + 4 (m_B + 1); diagonal H adds 0;
+    per PCG iteration bytes_B + 88 N; per extra apply bytes_B + 24 N."""
+    nnz = op.problem.a.nnz
+    N = op.dim
+    bytes_b = 12 * nnz + 4 * (op.m + 1)
+    return iters * (bytes_b + 88 * N) + applies * (bytes_b + 24 * N), bytes_b + 88 * N
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_baseline(op, rhs, iters: int):
+    """The reference path (oracle restatement, bit-identical to qpipm on the
+    golden vectors) on a bounded sample: `iters` PCG iterations of cfg5."""
+    from oracle import qp_oracle as orc
+    orc.jacobi_diagonal(op)              # warm the scipy views (not timed)
+    t0 = time.perf_counter()
+    res = orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=iters))
+    dt = time.perf_counter() - t0
+    # iterations + the final true-residual apply, as in the GPU step
+    return {"value": iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{iters} PCG iterations of cfg5 (+ Jacobi build + final apply), {dt:.1f} s; "
+                      f"numpy/scipy oracle bit-identical to qpipm; sparse matvecs single-threaded "
+                      f"({len(os.sched_getaffinity(0))} host cores visible)"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    problem, op, meta = make_workload(args.scale)
+    from oracle import qp_oracle as orc
+    rhs = meta["rhs"]
+    k_iter = args.ref_iters_per_step
+    orc.jacobi_diagonal(op)
+    for _ in range(args.warmup):
+        orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=k_iter))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=k_iter))
+    dt = time.perf_counter() - t0
+    value = k_iter * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg5 operator sweep 4Mx1M, 16 nnz/row, log10 w ~ U(-6,6)",
+                   "pcg_iters_per_step": k_iter, "seed": meta["seed"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
+                         "sample": f"{k_iter} PCG iterations per step of cfg5 through the oracle "
+                                   f"(numpy/scipy restatement of qpipm, bit-identical on golden vectors)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    from paper_2308_00637_b200 import _native
+    from paper_2308_00637_b200.direction import GpuKkt, gpu_direction, operator_for
+    from paper_2308_00637_b200.pcg import PcgConfig
+
+    problem, op, meta = make_workload(args.scale, seed=5 + rank)
+    rhs = meta["rhs"]
+    gk = GpuKkt(problem, op.bmap, device=local, scatter=args.scatter)
+    stream = torch.cuda.current_stream()
+    gk.ctx.call("qpk_set_stream", _native.ctypes.c_void_p(stream.cuda_stream))
+    gk.set_diagonals(op.d_diag, op.q_diag_extra)
+    gk.jacobi()
+    N = op.dim
+    rhs_d = torch.from_numpy(rhs).to(f"cuda:{local}")
+    x_d = torch.empty(N, dtype=torch.float64, device=f"cuda:{local}")
+    info = _native.PcgInfo()
+
+    def step():
+        gk.ctx.call("qpk_pcg_dev", rhs_d.data_ptr(), 1e-300, 1, args.iters, x_d.data_ptr(),
+                    _native.ctypes.byref(info), None)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    assert info.iterations == args.iters and info.applies == args.iters + 1, (info.iterations, info.applies)
+    barrier()
+    launches0 = gk.ctx.query("kernel_launches")
+    kernel_ms = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            kernel_ms.append(info.kernel_ms)
+        ev1.record(stream)
+        barrier()
+    launches = gk.ctx.query("kernel_launches") - launches0
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        t = torch.tensor([elapsed], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        elapsed = float(t.item())
+    total_iters = args.iters * args.steps * world
+    value = total_iters / elapsed
+
+    # e2e through the reference-facing drop-in, host buffers
+    e2e_cfg = PcgConfig(tol=1e-300, max_iters=args.iters)
+    gk_cached = operator_for(op, device=local)       # one upload per problem (not timed)
+    gpu_direction(op, rhs, e2e_cfg)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        res = gpu_direction(op, rhs, e2e_cfg)
+        _ = float(res.final_residual_norm)
+    barrier()
+    e2e_dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_dt], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_dt = float(t.item())
+    e2e_value = args.iters * e2e_steps * world / e2e_dt
+    h2d = 8 * (op.m + op.n + N)
+    d2h = 8 * N
+
+    # roofline of the dominant kernel (the persistent PCG kernel: one launch per step)
+    per_launch, per_iter = algorithmic_bytes(op, args.iters, applies=1)
+    avg_ms = float(np.mean(kernel_ms))
+    achieved = per_launch / (avg_ms * 1e-3) / 1e9
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    traffic = None
+    prof = ROOT / "profiles" / "r01_pcg_kernel_dram.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator of BASELINE.json configs[4]; no dataset involved)",
+            "config": {"workload": f"cfg5 operator sweep {op.m}x{op.n}, 16 nnz/row, H=diag(U(1e-2,1)), "
+                                   f"log10 w ~ U(-6,6); {args.iters} PCG iterations per step",
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "scatter": "atomic" if args.scatter == 1 else "csc",
+                       "l2": "inputs larger than L2 (B alone 0.78 GB vs 126 MB L2)",
+                       "grid": gk.ctx.query("grid"), "lanes_per_row": gk.ctx.query("lanes"),
+                       "seed": meta["seed"]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": per_launch, "algorithmic_bytes_per_iter": per_iter,
+                         "kernel": "pcg_kernel<4,false>", "kernel_ms_avg": avg_ms,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "gpu_direction(op, rhs, PcgConfig) host buffers"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(op, rhs, args.cpu_iters)
+        print(json.dumps(line), flush=True)
+    gk.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+/*
+ * qpk.h -- C ABI of libqpk.so, the B200 (sm_100a) Jacobi-PCG direction
+ * solver for the Forsgren-Gill doubly augmented KKT system
+ *
+ *     K = [[Q + 2 B' D^-1 B, B'], [B, D]],   Q = H + diag(q_extra),
+ *     B = (C; A_l; -A_u),  D = diag(d_diag)
+ *
+ * It is the native side of the reference's direction-solver hook
+ *     DirectionSolver = Callable[[KktOperator, ndarray, PcgConfig], PcgResult]
+ *     (/root/reference/pkg/src/qpipm/ipm.py:176, called at ipm.py:206)
+ * and replaces, function by function:
+ *     qpk_problem_begin, _add_rows, qpk_set_hessian_<kind>, _finalize
+ *                           -> the per-problem data of KktOperator
+ *                              (kkt.py:146-160, 203-208; model.py:17-162);
+ *                              B is uploaded once per problem instead of the
+ *                              row_submatrix copies made each IPM iteration
+ *     qpk_set_diagonals     -> build_operator's d_diag / q_diag_extra
+ *                              (kkt.py:190-202), once per IPM iteration
+ *     qpk_jacobi            -> jacobi_diagonal (kkt.py:224-239) and the
+ *                              inv_diag of _pcg_direction (ipm.py:180)
+ *     qpk_apply             -> apply_doubly_augmented (kkt.py:211-221)
+ *     qpk_pcg               -> pcg(apply_op, apply_prec, rhs, cfg)
+ *                              (linalg.py:66-133) with x0 = 0, as
+ *                              _pcg_direction calls it (ipm.py:181-182)
+ *
+ * Conventions: every function returns QPK_OK (0) or a negative QPK_E* code;
+ * qpk_last_error() returns a thread-local message for the last failure.
+ * Pointers are HOST pointers unless the function name ends in _dev, in which
+ * case they are device pointers on the context's device.  All sizes are
+ * element counts.  Not reentrant per context (one caller thread, as the
+ * reference).  A breakdown (p'Kp <= 0, linalg.py:102-103) is not
+ * an error: qpk_pcg returns QPK_OK with info.status == QPK_PCG_BREAKDOWN and
+ * the best iterate in x (the reference raises PcgBreakdownError carrying the
+ * same result).
+ */
+#ifndef QPK_H
+#define QPK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QPK_ABI_VERSION 1
+
+enum {
+  QPK_OK = 0,
+  QPK_E_ARG = -1,      /* invalid argument / dimension (reference DimensionError) */
+  QPK_E_STATE = -2,    /* call out of order (e.g. qpk_pcg before qpk_set_diagonals) */
+  QPK_E_CUDA = -3,     /* CUDA runtime failure */
+  QPK_E_NOMEM = -4,    /* device or host allocation failed */
+  QPK_E_UNSUPPORTED = -5
+};
+
+enum { QPK_HESS_DIAG = 0, QPK_HESS_CSR = 1, QPK_HESS_DENSE = 2, QPK_HESS_LOWRANK = 3 };
+
+enum { QPK_PCG_OK = 0, QPK_PCG_BREAKDOWN = 1 };
+
+/* scatter strategy for the B' z product of the operator apply */
+enum {
+  QPK_SCATTER_AUTO = 0,    /* chosen per matrix at finalize */
+  QPK_SCATTER_ATOMIC = 1,  /* one pass over B, fp64 atomics (order not reproducible) */
+  QPK_SCATTER_CSC = 2      /* second, gather-only pass over a resident CSC copy:
+                              bitwise reproducible run to run */
+};
+
+typedef struct qpk_ctx qpk_ctx;
+
+/* result record of qpk_pcg: PcgResult (linalg.py:42-47) plus diagnostics */
+typedef struct {
+  int32_t iterations;          /* PcgResult.iterations */
+  int32_t converged;           /* PcgResult.converged */
+  int32_t status;              /* QPK_PCG_OK or QPK_PCG_BREAKDOWN */
+  int32_t restarts;            /* true-residual restarts (linalg.py:117-125) */
+  int32_t applies;             /* operator applications performed */
+  int32_t reserved;
+  double final_residual_norm;  /* PcgResult.final_residual_norm (true residual,
+                                  or best recurrence residual on breakdown) */
+  double threshold;            /* tol * ||rhs|| (relative) or tol */
+  double rhs_norm;             /* ||rhs|| */
+  double kernel_ms;            /* device time of the solve (CUDA events) */
+} qpk_pcg_info;
+
+int qpk_abi_version(void);
+const char* qpk_last_error(void);
+
+/* one context per device (one process per GPU) */
+int qpk_create(int device, qpk_ctx** out);
+int qpk_destroy(qpk_ctx* ctx);
+/* use an external cudaStream_t (e.g. torch's current stream); NULL = own stream */
+int qpk_set_stream(qpk_ctx* ctx, void* stream);
+int qpk_synchronize(qpk_ctx* ctx);
+
+/* ---- problem upload (once per QpProblem) ------------------------------ */
+/* n variables; m_e equality rows (C), m_l rows of A with a finite lower bound,
+ * m_u rows of A with a finite upper bound; m_B = m_e + m_l + m_u. */
+int qpk_problem_begin(qpk_ctx* ctx, int64_t n, int64_t m_e, int64_t m_l, int64_t m_u);
+/* Append rows to B in reference order (C, then A_l, then A_u with sign = -1).
+ * row_offsets/col_indices/values: a CSR matrix (int64 offsets and columns as
+ * SparseMatrix stores them, model.py:30-33); rows: the row indices of that
+ * matrix to append, in order (NULL = all n_rows rows). */
+int qpk_problem_add_rows(qpk_ctx* ctx, int64_t n_rows, const int64_t* row_offsets,
+                         const int64_t* col_indices, const double* values,
+                         const int64_t* rows, int64_t n_sel, double sign);
+int qpk_set_hessian_diag(qpk_ctx* ctx, const double* d);
+int qpk_set_hessian_csr(qpk_ctx* ctx, const int64_t* row_offsets, const int64_t* col_indices,
+                        const double* values);
+int qpk_set_hessian_dense(qpk_ctx* ctx, const double* m_rowmajor);
+int qpk_set_hessian_lowrank(qpk_ctx* ctx, const double* h0, int64_t k, const double* u_rowmajor,
+                            const double* w);
+/* builds the device layout; scatter = QPK_SCATTER_* */
+int qpk_problem_finalize(qpk_ctx* ctx, int scatter);
+
+/* ---- per IPM iteration --------------------------------------------------- */
+int qpk_set_diagonals(qpk_ctx* ctx, const double* d_diag, const double* q_extra);
+int qpk_set_diagonals_dev(qpk_ctx* ctx, const double* d_diag, const double* q_extra);
+/* builds the Jacobi diagonal on the device; diag_out (length n+m_B, nullable) receives it */
+int qpk_jacobi(qpk_ctx* ctx, double* diag_out);
+
+/* y = K v (length n + m_B) */
+int qpk_apply(qpk_ctx* ctx, const double* v, double* y);
+int qpk_apply_dev(qpk_ctx* ctx, const double* v, double* y);
+
+/* PCG from x0 = 0.  resid_hist (nullable, length max_iters + 1) receives the
+ * recurrence residual norm after each iteration k (index k; index 0 = ||rhs||);
+ * entries past info.iterations are untouched. */
+int qpk_pcg(qpk_ctx* ctx, const double* rhs, double tol, int tol_is_relative, int64_t max_iters,
+            double* x, qpk_pcg_info* info, double* resid_hist);
+int qpk_pcg_dev(qpk_ctx* ctx, const double* rhs, double tol, int tol_is_relative, int64_t max_iters,
+                double* x, qpk_pcg_info* info, double* resid_hist_dev);
+
+/* ---- introspection ------------------------------------------------------ */
+/* keys: "n", "m", "nnz", "nnz_padded", "lanes", "scatter", "grid", "block",
+ * "sms", "hess_kind", "device_bytes", "kernel_launches" */
+int64_t qpk_query(qpk_ctx* ctx, const char* key);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QPK_H */

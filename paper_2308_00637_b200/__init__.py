@@ -1,0 +1,11 @@
+"""B200-native Jacobi-PCG direction solver for the doubly augmented KKT system.
+
+Drop-in for the linear-solver hook of the reference interior-point QP solver
+(qpipm, arXiv 2308.00637): ``solve(problem, cfg, direction_solver=gpu_direction)``.
+"""
+
+from .direction import GpuKkt, gpu_direction, operator_for
+from .pcg import PcgBreakdownError, PcgConfig, PcgResult
+
+__all__ = ["GpuKkt", "gpu_direction", "operator_for", "PcgBreakdownError", "PcgConfig", "PcgResult"]
+__version__ = "0.1.0"

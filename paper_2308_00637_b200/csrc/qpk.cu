@@ -1,0 +1,861 @@
+// qpk.cu -- libqpk.so: B200-native Jacobi-PCG on the doubly augmented KKT
+// system, behind the C ABI declared in include/qpk.h.
+//
+// Kernels
+//   pcg_kernel<L, CSC>   persistent cooperative kernel running the whole PCG
+//                        solve of linalg.py:66-133 on the device (one launch
+//                        per solve, grid.sync between phases, no host round
+//                        trips); L = lanes per row of B, CSC = gather-only
+//                        (deterministic) B'z.
+//   k_prep / k_rows / k_finish   the same phases as standalone launches, for
+//                        qpk_apply (apply_doubly_augmented, kkt.py:211-221)
+//   k_jac_*              jacobi_diagonal (kkt.py:224-239) + inv_diag (ipm.py:180)
+//   k_hdiag_*            hessian_diagonal (model.py:179-186), once per problem
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/qpk.h"
+#include "qpk_device.cuh"
+
+namespace cg = cooperative_groups;
+using namespace qpk;
+
+// =========================================================== device code ===
+struct PcgOut {
+  int iterations, converged, status, restarts, applies, result_buf;
+  double final_norm, threshold, rhs_norm;
+};
+
+struct PcgParams {
+  Op op;
+  const double* rhs;
+  double* x0; double* x1; double* x2;
+  double* r; double* p; double* y; double* zb;
+  const double* minv;
+  double* part; int G;
+  double tol; int rel; long long max_iters;
+  double* hist;
+  PcgOut* out;
+};
+
+__device__ __forceinline__ void write_out(const PcgParams& P, long long iters, int conv, int status,
+                                          int restarts, int applies, int buf, double fin, double thr,
+                                          double rhs_norm) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    P.out->iterations = (int)iters; P.out->converged = conv; P.out->status = status;
+    P.out->restarts = restarts; P.out->applies = applies; P.out->result_buf = buf;
+    P.out->final_norm = fin; P.out->threshold = thr; P.out->rhs_norm = rhs_norm;
+  }
+}
+
+// p = z (+ beta p), z = minv * r ; then prep(p) for the next apply.
+// Partial sums: SLOT_AUX = r'z, SLOT_PREP = p'(diag Q)p, SLOT_S.. = U'p.
+__device__ void phase_direction(const PcgParams& P, double beta, bool restart, double* red) {
+  const Op& op = P.op;
+  const int N = op.n + op.m, G = P.G;
+  double rz = 0.0, acc = 0.0;
+  double sacc[QPK_KMAX];
+  const bool lr = op.H.kind == HESS_LOWRANK;
+  if (lr) for (int kk = 0; kk < op.H.k; ++kk) sacc[kk] = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const double ri = P.r[i];
+    const double zi = __dmul_rn(__ldg(P.minv + i), ri);
+    rz += ri * zi;
+    const double pi = restart ? zi : __dadd_rn(zi, __dmul_rn(beta, P.p[i]));
+    P.p[i] = pi;
+    if (i < op.n) {
+      acc += prep_elem(op, i, pi, P.y);
+      if (lr) lowrank_accum(op, i, pi, sacc);
+    }
+  }
+  double t = block_sum(rz, red);
+  if (threadIdx.x == 0) P.part[SLOT_AUX * G + blockIdx.x] = t;
+  t = block_sum(acc, red);
+  if (threadIdx.x == 0) P.part[SLOT_PREP * G + blockIdx.x] = t;
+  if (lr) lowrank_flush(op, sacc, P.part, G, red);
+}
+
+template <int L, bool CSC>
+__global__ void __launch_bounds__(QPK_BLOCK) pcg_kernel(PcgParams P) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[32];
+  __shared__ double s_lr[QPK_KMAX];
+  const Op& op = P.op;
+  const int N = op.n + op.m, G = P.G;
+  double* xs[3] = {P.x0, P.x1, P.x2};
+  const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+
+  // x = 0, r = rhs (linalg.py:85-87), ||rhs||
+  {
+    double acc = 0.0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+      const double b = __ldg(P.rhs + i);
+      P.x0[i] = 0.0;
+      P.r[i] = b;
+      acc += b * b;
+    }
+    const double t = block_sum(acc, red);
+    if (threadIdx.x == 0) P.part[SLOT_AUX * G + blockIdx.x] = t;
+  }
+  grid.sync();
+  const double rhs_norm = sqrt(grid_total(P.part + SLOT_AUX * G, G, red));
+  const double thr = P.rel ? P.tol * rhs_norm : P.tol;          // linalg.py:83
+  double rnorm = rhs_norm, best_rnorm = rhs_norm;
+  int cur = 0, best = 0, restarts = 0, applies = 0;
+  if (writer && P.hist) P.hist[0] = rnorm;
+  if (rnorm <= thr) {                                               // linalg.py:93-94
+    write_out(P, 0, 1, QPK_PCG_OK, 0, 0, 0, rnorm, thr, rhs_norm);
+    return;
+  }
+  phase_direction(P, 0.0, true, red);                               // z, p = z, r'z
+  grid.sync();
+  double rz = grid_total(P.part + SLOT_AUX * G, G, red);
+
+  for (long long k = 1; k <= P.max_iters; ++k) {
+    // y = K p  (+ p'Kp)
+    phase_rows<L, CSC>(op, P.p, P.y, P.zb, P.part, G, red, s_lr);
+    ++applies;
+    grid.sync();
+    const double pap = grid_total(P.part + SLOT_ROWS * G, G, red) + grid_total(P.part + SLOT_PREP * G, G, red);
+    if (pap <= 0.0) {                                               // linalg.py:102-103
+      write_out(P, k - 1, 0, QPK_PCG_BREAKDOWN, restarts, applies, best, best_rnorm, thr, rhs_norm);
+      return;
+    }
+    const double alpha = rz / pap;
+    const int xn = (cur != best) ? 3 - cur - best : (cur + 1) % 3;
+    {
+      const double* xc = xs[cur];
+      double* xw = xs[xn];
+      double rr = 0.0, rzn = 0.0;
+      for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
+        xw[i] = __dadd_rn(xc[i], __dmul_rn(alpha, P.p[i]));       // x += alpha p
+        const double ri = __dsub_rn(P.r[i], __dmul_rn(alpha, yi));  // r -= alpha op_p
+        P.r[i] = ri;
+        const double zi = __dmul_rn(__ldg(P.minv + i), ri);
+        rr += ri * ri;
+        rzn += ri * zi;
+      });
+      double t = block_sum(rr, red);
+      if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
+      t = block_sum(rzn, red);
+      if (threadIdx.x == 0) P.part[SLOT_RZ * G + blockIdx.x] = t;
+    }
+    grid.sync();
+    cur = xn;
+    rnorm = sqrt(grid_total(P.part + SLOT_RR * G, G, red));
+    if (writer && P.hist) P.hist[k] = rnorm;
+    if (rnorm < best_rnorm) { best = cur; best_rnorm = rnorm; }     // linalg.py:110-111
+    if (rnorm <= thr) {
+      // explicit residual rhs - K x (linalg.py:112-116)
+      phase_prep(op, xs[cur], P.y, P.part, G, red);
+      grid.sync();
+      phase_rows<L, CSC>(op, xs[cur], P.y, P.zb, P.part, G, red, s_lr);
+      ++applies;
+      grid.sync();
+      {
+        double rr = 0.0;
+        for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
+          const double ri = __dsub_rn(__ldg(P.rhs + i), yi);
+          P.r[i] = ri;
+          rr += ri * ri;
+        });
+        const double t = block_sum(rr, red);
+        if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
+      }
+      grid.sync();
+      const double true_norm = sqrt(grid_total(P.part + SLOT_RR * G, G, red));
+      if (true_norm <= thr) {
+        write_out(P, k, 1, QPK_PCG_OK, restarts, applies, cur, true_norm, thr, rhs_norm);
+        return;
+      }
+      // recurrence drifted: restart from the explicit residual (linalg.py:117-125)
+      ++restarts;
+      rnorm = true_norm;
+      if (rnorm < best_rnorm) { best = cur; best_rnorm = rnorm; }
+      phase_direction(P, 0.0, true, red);
+      grid.sync();
+      rz = grid_total(P.part + SLOT_AUX * G, G, red);
+      continue;
+    }
+    const double rz_next = grid_total(P.part + SLOT_RZ * G, G, red);  // linalg.py:126-130
+    const double beta = rz_next / rz;
+    rz = rz_next;
+    phase_direction(P, beta, false, red);
+    grid.sync();
+  }
+  // iteration cap: true residual of the best iterate (linalg.py:132-133)
+  phase_prep(op, xs[best], P.y, P.part, G, red);
+  grid.sync();
+  phase_rows<L, CSC>(op, xs[best], P.y, P.zb, P.part, G, red, s_lr);
+  ++applies;
+  grid.sync();
+  {
+    double rr = 0.0;
+    for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
+      const double ri = __dsub_rn(__ldg(P.rhs + i), yi);
+      rr += ri * ri;
+    });
+    const double t = block_sum(rr, red);
+    if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
+  }
+  grid.sync();
+  const double true_norm = sqrt(grid_total(P.part + SLOT_RR * G, G, red));
+  write_out(P, P.max_iters, true_norm <= thr ? 1 : 0, QPK_PCG_OK, restarts, applies, best, true_norm, thr,
+            rhs_norm);
+}
+
+// ---------------------------------------------------- standalone phases ---
+__global__ void __launch_bounds__(QPK_BLOCK) k_prep(Op op, const double* v, double* y, double* part, int G) {
+  __shared__ double red[32];
+  phase_prep(op, v, y, part, G, red);
+}
+
+template <int L, bool CSC>
+__global__ void __launch_bounds__(QPK_BLOCK) k_rows(Op op, const double* v, double* y, double* zb, double* part, int G) {
+  __shared__ double red[32];
+  __shared__ double s_lr[QPK_KMAX];
+  phase_rows<L, CSC>(op, v, y, zb, part, G, red, s_lr);
+}
+
+__global__ void __launch_bounds__(QPK_BLOCK) k_finish_csc(Op op, double* y, const double* zb) {
+  for_each_final<true>(op, y, zb, [&](int i, double yi) { if (i < op.n) y[i] = yi; });
+}
+
+// Jacobi: acc_j = sum_r B_rj^2 * (1/d_r)
+template <int L>
+__global__ void __launch_bounds__(QPK_BLOCK) k_jac_rows(Op op, double* acc) {
+  const int lane = threadIdx.x & (L - 1);
+  const long long sub = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / L;
+  const long long nsub = ((long long)gridDim.x * blockDim.x) / L;
+  for (long long r = sub; r < op.m; r += nsub) {
+    const double dinv = 1.0 / __ldg(op.d + r);
+    const int b = __ldg(op.rp + r), e = __ldg(op.rp + r + 1);
+    for (int k = b + 4 * lane; k < e; k += 4 * L) {
+      int4 c = ld_stream_i4(op.ci + k);
+      double2 a0 = ld_stream_d2(op.bv + k), a1 = ld_stream_d2(op.bv + k + 2);
+      if (c.x >= 0) atomicAdd(acc + c.x, __dmul_rn(a0.x, a0.x) * dinv);
+      if (c.y >= 0) atomicAdd(acc + c.y, __dmul_rn(a0.y, a0.y) * dinv);
+      if (c.z >= 0) atomicAdd(acc + c.z, __dmul_rn(a1.x, a1.x) * dinv);
+      if (c.w >= 0) atomicAdd(acc + c.w, __dmul_rn(a1.y, a1.y) * dinv);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(QPK_BLOCK) k_jac_cols(Op op, double* acc) {
+  const int LC = op.csc_lanes, lc = threadIdx.x & (LC - 1);
+  const int per = 32 / LC, sw = (threadIdx.x & 31) / LC;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
+    const int j = (int)jb + sw;
+    double s = 0.0;
+    if (j < op.n) {
+      const int b = __ldg(op.cp + j), e = __ldg(op.cp + j + 1);
+      for (int k = b + lc; k < e; k += LC) {
+        const double a = __ldg(op.cv + k);
+        s += __dmul_rn(a, a) * (1.0 / __ldg(op.d + __ldg(op.ri + k)));
+      }
+    }
+    for (int o = LC / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (j < op.n && lc == 0) acc[j] = s;
+  }
+}
+
+// jac = (diag(H) + q_extra) + 2 acc ; D   and   minv = 1 / jac
+__global__ void k_jac_finish(Op op, const double* hdiag, const double* acc, double* jac, double* minv) {
+  const int N = op.n + op.m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    double v;
+    if (i < op.n) v = __dadd_rn(__dadd_rn(__ldg(hdiag + i), __ldg(op.q + i)), __dmul_rn(2.0, acc[i]));
+    else v = __ldg(op.d + (i - op.n));
+    jac[i] = v;
+    minv[i] = 1.0 / v;
+  }
+}
+
+// diag(H) once per problem (model.py:179-186)
+__global__ void k_hdiag(Hess H, int n, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    double v = 0.0;
+    if (H.kind == HESS_DIAG) v = H.h[j];
+    else if (H.kind == HESS_DENSE) v = H.dense[(size_t)j * n + j];
+    else if (H.kind == HESS_CSR) {
+      for (int k = H.rp[j]; k < H.rp[j + 1]; ++k)
+        if (H.ci[k] == j) { v = H.v[k]; break; }
+    } else {
+      double s = 0.0;
+      const double* urow = H.U + (size_t)j * H.k;
+      for (int kk = 0; kk < H.k; ++kk) s += H.w[kk] * (urow[kk] * urow[kk]);
+      v = H.h[j] + s;
+    }
+    out[j] = v;
+  }
+}
+
+// ============================================================= host side ===
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess) return fail(QPK_E_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                       __FILE__, __LINE__);                                  \
+  } while (0)
+
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() { if (p) cudaFree(p); p = nullptr; n = 0; }
+  cudaError_t alloc(size_t count) {
+    if (count <= n && p) return cudaSuccess;
+    release();
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) n = count; else p = nullptr;
+    return e;
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+int pow2_clamp(long long v, int lo, int hi) {
+  int p = 1;
+  while (p < v && p < hi) p <<= 1;
+  return std::max(lo, std::min(hi, p));
+}
+
+}  // namespace
+
+struct qpk_ctx {
+  int device = 0;
+  int sms = 0;
+  cudaStream_t own = nullptr, stream = nullptr;
+  long long launches = 0;
+
+  // problem staging
+  bool building = false, finalized = false;
+  long long n = 0, m = 0, m_e = 0, m_l = 0, m_u = 0;
+  std::vector<int> h_rp;
+  std::vector<int> h_ci;
+  std::vector<double> h_v;
+  long long nnz = 0;
+
+  int hkind = -1;
+  long long hk = 0;
+  std::vector<double> h_h;               // diag d / low-rank h0
+  std::vector<int> h_hrp, h_hci; std::vector<double> h_hv;
+  std::vector<double> h_dense, h_U, h_w;
+
+  int scatter = QPK_SCATTER_ATOMIC;
+  int lanes = 4, csc_lanes = 8, h_lanes = 8;
+
+  // device problem
+  DBuf<int> rp, ci, cp, ri, hrp, hci;
+  DBuf<double> bv, cv, hh, hv, hdense, U, w, hdiag;
+  bool have_csc = false;
+
+  // per IPM iteration
+  DBuf<double> d, q, jac, minv;
+  bool diag_set = false, jac_ready = false;
+
+  // work
+  DBuf<double> x[3], r, p, y, zb, rhs, part, hist, vin;
+  DBuf<PcgOut> out;
+  int grid_pcg = 0, grid_std = 0;
+
+  Op op() const {
+    Op o;
+    o.n = (int)n; o.m = (int)m;
+    o.rp = rp.p; o.ci = ci.p; o.bv = bv.p;
+    o.cp = cp.p; o.ri = ri.p; o.cv = cv.p; o.csc_lanes = csc_lanes;
+    o.H.kind = hkind; o.H.h = hh.p; o.H.rp = hrp.p; o.H.ci = hci.p; o.H.v = hv.p; o.H.lanes = h_lanes;
+    o.H.dense = hdense.p; o.H.U = U.p; o.H.w = w.p; o.H.k = (int)hk;
+    o.d = d.p; o.q = q.p;
+    return o;
+  }
+  long long N() const { return n + m; }
+};
+
+template <typename T>
+static cudaError_t upload(DBuf<T>& dst, const std::vector<T>& src, cudaStream_t s) {
+  cudaError_t e = dst.alloc(src.size());
+  if (e != cudaSuccess || src.empty()) return e;
+  return cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
+// ---------------------------------------------------------- dispatchers ---
+template <int L, bool CSC>
+static const void* pcg_fn() { return (const void*)pcg_kernel<L, CSC>; }
+
+static const void* pcg_kernel_for(int lanes, bool csc) {
+  switch (lanes) {
+    case 1: return csc ? pcg_fn<1, true>() : pcg_fn<1, false>();
+    case 2: return csc ? pcg_fn<2, true>() : pcg_fn<2, false>();
+    case 4: return csc ? pcg_fn<4, true>() : pcg_fn<4, false>();
+    case 8: return csc ? pcg_fn<8, true>() : pcg_fn<8, false>();
+    case 16: return csc ? pcg_fn<16, true>() : pcg_fn<16, false>();
+    default: return csc ? pcg_fn<32, true>() : pcg_fn<32, false>();
+  }
+}
+
+template <bool CSC>
+static void launch_rows(int lanes, int grid, cudaStream_t s, const Op& o, const double* v, double* y, double* zb,
+                        double* part, int G) {
+  switch (lanes) {
+    case 1: k_rows<1, CSC><<<grid, QPK_BLOCK, 0, s>>>(o, v, y, zb, part, G); break;
+    case 2: k_rows<2, CSC><<<grid, QPK_BLOCK, 0, s>>>(o, v, y, zb, part, G); break;
+    case 4: k_rows<4, CSC><<<grid, QPK_BLOCK, 0, s>>>(o, v, y, zb, part, G); break;
+    case 8: k_rows<8, CSC><<<grid, QPK_BLOCK, 0, s>>>(o, v, y, zb, part, G); break;
+    case 16: k_rows<16, CSC><<<grid, QPK_BLOCK, 0, s>>>(o, v, y, zb, part, G); break;
+    default: k_rows<32, CSC><<<grid, QPK_BLOCK, 0, s>>>(o, v, y, zb, part, G); break;
+  }
+}
+
+static void launch_jac_rows(int lanes, int grid, cudaStream_t s, const Op& o, double* acc) {
+  switch (lanes) {
+    case 1: k_jac_rows<1><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+    case 2: k_jac_rows<2><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+    case 4: k_jac_rows<4><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+    case 8: k_jac_rows<8><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+    case 16: k_jac_rows<16><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+    default: k_jac_rows<32><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+  }
+}
+
+// ------------------------------------------------------------------ ABI ---
+extern "C" {
+
+int qpk_abi_version(void) { return QPK_ABI_VERSION; }
+const char* qpk_last_error(void) { return g_err.c_str(); }
+
+int qpk_create(int device, qpk_ctx** out) {
+  if (!out) return fail(QPK_E_ARG, "qpk_create: out is NULL");
+  int count = 0;
+  CUDA_TRY(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) return fail(QPK_E_ARG, "qpk_create: device %d of %d", device, count);
+  CUDA_TRY(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (!prop.cooperativeLaunch) return fail(QPK_E_UNSUPPORTED, "device %d lacks cooperative launch", device);
+  qpk_ctx* c = new (std::nothrow) qpk_ctx();
+  if (!c) return fail(QPK_E_NOMEM, "qpk_create: host allocation failed");
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) { delete c; return fail(QPK_E_CUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)); }
+  c->stream = c->own;
+  if (c->out.alloc(1) != cudaSuccess) { delete c; return fail(QPK_E_NOMEM, "qpk_create: device alloc"); }
+  *out = c;
+  return QPK_OK;
+}
+
+int qpk_destroy(qpk_ctx* c) {
+  if (!c) return QPK_OK;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  if (c->own) cudaStreamDestroy(c->own);
+  delete c;
+  return QPK_OK;
+}
+
+int qpk_set_stream(qpk_ctx* c, void* stream) {
+  if (!c) return fail(QPK_E_ARG, "null context");
+  c->stream = stream ? (cudaStream_t)stream : c->own;
+  return QPK_OK;
+}
+
+int qpk_synchronize(qpk_ctx* c) {
+  if (!c) return fail(QPK_E_ARG, "null context");
+  CUDA_TRY(cudaSetDevice(c->device));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+int qpk_problem_begin(qpk_ctx* c, int64_t n, int64_t m_e, int64_t m_l, int64_t m_u) {
+  if (!c) return fail(QPK_E_ARG, "null context");
+  if (n < 1 || m_e < 0 || m_l < 0 || m_u < 0)
+    return fail(QPK_E_ARG, "qpk_problem_begin: bad sizes n=%lld m_e=%lld m_l=%lld m_u=%lld", (long long)n,
+                (long long)m_e, (long long)m_l, (long long)m_u);
+  if (n + m_e + m_l + m_u >= (1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "dimension exceeds int32 range");
+  c->building = true; c->finalized = false; c->diag_set = false; c->jac_ready = false; c->have_csc = false;
+  c->n = n; c->m_e = m_e; c->m_l = m_l; c->m_u = m_u; c->m = 0;
+  c->h_rp.assign(1, 0); c->h_ci.clear(); c->h_v.clear(); c->nnz = 0;
+  c->hkind = -1; c->hk = 0;
+  return QPK_OK;
+}
+
+int qpk_problem_add_rows(qpk_ctx* c, int64_t n_rows, const int64_t* ro, const int64_t* ci, const double* vals,
+                         const int64_t* rows, int64_t n_sel, double sign) {
+  if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_add_rows: no problem being built");
+  if (n_rows < 0 || !ro || (n_rows > 0 && (!ci && ro[n_rows] > 0)))
+    return fail(QPK_E_ARG, "qpk_problem_add_rows: bad CSR");
+  const int64_t count = rows ? n_sel : n_rows;
+  const long long mB = c->m_e + c->m_l + c->m_u;
+  if (c->m + count > mB) return fail(QPK_E_ARG, "qpk_problem_add_rows: more rows than m_B=%lld", mB);
+  for (int64_t s = 0; s < count; ++s) {
+    const int64_t i = rows ? rows[s] : s;
+    if (i < 0 || i >= n_rows) return fail(QPK_E_ARG, "qpk_problem_add_rows: row index %lld out of range", (long long)i);
+    const int64_t b = ro[i], e = ro[i + 1];
+    if (e < b) return fail(QPK_E_ARG, "row_offsets must be nondecreasing");
+    for (int64_t k = b; k < e; ++k) {
+      const int64_t col = ci[k];
+      if (col < 0 || col >= c->n) return fail(QPK_E_ARG, "column index %lld out of range", (long long)col);
+      c->h_ci.push_back((int)col);
+      c->h_v.push_back(sign * vals[k]);
+    }
+    c->nnz += e - b;
+    while (c->h_ci.size() & 3) { c->h_ci.push_back(-1); c->h_v.push_back(0.0); }
+    if (c->h_ci.size() >= (size_t)(1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "nnz exceeds int32 range");
+    c->h_rp.push_back((int)c->h_ci.size());
+    c->m += 1;
+  }
+  return QPK_OK;
+}
+
+int qpk_set_hessian_diag(qpk_ctx* c, const double* dd) {
+  if (!c || !c->building || !dd) return fail(QPK_E_STATE, "qpk_set_hessian_diag: bad state/arg");
+  c->hkind = QPK_HESS_DIAG;
+  c->h_h.assign(dd, dd + c->n);
+  return QPK_OK;
+}
+
+int qpk_set_hessian_csr(qpk_ctx* c, const int64_t* ro, const int64_t* ci, const double* v) {
+  if (!c || !c->building || !ro) return fail(QPK_E_STATE, "qpk_set_hessian_csr: bad state/arg");
+  const int64_t nnz = ro[c->n];
+  if (nnz >= (1LL << 31)) return fail(QPK_E_UNSUPPORTED, "Hessian nnz exceeds int32 range");
+  c->hkind = QPK_HESS_CSR;
+  c->h_hrp.resize(c->n + 1);
+  for (long long j = 0; j <= c->n; ++j) c->h_hrp[j] = (int)ro[j];
+  c->h_hci.resize(nnz);
+  c->h_hv.assign(v, v + nnz);
+  for (int64_t k = 0; k < nnz; ++k) {
+    if (ci[k] < 0 || ci[k] >= c->n) return fail(QPK_E_ARG, "Hessian column out of range");
+    c->h_hci[k] = (int)ci[k];
+  }
+  c->h_lanes = pow2_clamp((nnz + c->n - 1) / std::max<long long>(c->n, 1), 1, 32);
+  return QPK_OK;
+}
+
+int qpk_set_hessian_dense(qpk_ctx* c, const double* mm) {
+  if (!c || !c->building || !mm) return fail(QPK_E_STATE, "qpk_set_hessian_dense: bad state/arg");
+  c->hkind = QPK_HESS_DENSE;
+  c->h_dense.assign(mm, mm + c->n * c->n);
+  return QPK_OK;
+}
+
+int qpk_set_hessian_lowrank(qpk_ctx* c, const double* h0, int64_t k, const double* u, const double* w) {
+  if (!c || !c->building || !h0 || k < 0) return fail(QPK_E_STATE, "qpk_set_hessian_lowrank: bad state/arg");
+  if (k > QPK_KMAX) return fail(QPK_E_UNSUPPORTED, "low-rank Hessian with k=%lld > %d", (long long)k, QPK_KMAX);
+  c->hkind = QPK_HESS_LOWRANK;
+  c->hk = k;
+  c->h_h.assign(h0, h0 + c->n);
+  c->h_U.assign(u, u + c->n * k);
+  c->h_w.assign(w, w + k);
+  return QPK_OK;
+}
+
+static int build_csc(qpk_ctx* c) {
+  const long long n = c->n;
+  std::vector<int> cp(n + 1, 0);
+  for (int col : c->h_ci) if (col >= 0) cp[col + 1]++;
+  for (long long j = 0; j < n; ++j) cp[j + 1] += cp[j];
+  std::vector<int> ri(c->nnz);
+  std::vector<double> cv(c->nnz);
+  std::vector<int> pos(cp.begin(), cp.end() - 1);
+  for (long long r = 0; r < c->m; ++r)
+    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+      const int col = c->h_ci[k];
+      if (col < 0) continue;
+      const int at = pos[col]++;
+      ri[at] = (int)r;
+      cv[at] = c->h_v[k];
+    }
+  CUDA_TRY(upload(c->cp, cp, c->stream));
+  CUDA_TRY(upload(c->ri, ri, c->stream));
+  CUDA_TRY(upload(c->cv, cv, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  c->csc_lanes = pow2_clamp((c->nnz + n - 1) / std::max<long long>(n, 1) / 2, 1, 32);
+  c->have_csc = true;
+  return QPK_OK;
+}
+
+int qpk_problem_finalize(qpk_ctx* c, int scatter) {
+  if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_finalize: no problem being built");
+  const long long mB = c->m_e + c->m_l + c->m_u;
+  if (c->m != mB) return fail(QPK_E_ARG, "qpk_problem_finalize: %lld rows added, m_B=%lld", c->m, mB);
+  if (c->hkind < 0) return fail(QPK_E_STATE, "qpk_problem_finalize: Hessian not set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  CUDA_TRY(upload(c->rp, c->h_rp, s));
+  CUDA_TRY(upload(c->ci, c->h_ci, s));
+  CUDA_TRY(upload(c->bv, c->h_v, s));
+  if (c->hkind == QPK_HESS_DIAG || c->hkind == QPK_HESS_LOWRANK) CUDA_TRY(upload(c->hh, c->h_h, s));
+  if (c->hkind == QPK_HESS_CSR) {
+    CUDA_TRY(upload(c->hrp, c->h_hrp, s));
+    CUDA_TRY(upload(c->hci, c->h_hci, s));
+    CUDA_TRY(upload(c->hv, c->h_hv, s));
+  }
+  if (c->hkind == QPK_HESS_DENSE) CUDA_TRY(upload(c->hdense, c->h_dense, s));
+  if (c->hkind == QPK_HESS_LOWRANK) {
+    CUDA_TRY(upload(c->U, c->h_U, s));
+    CUDA_TRY(upload(c->w, c->h_w, s));
+  }
+  const long long N = c->N();
+  CUDA_TRY(c->hdiag.alloc(c->n));
+  CUDA_TRY(c->d.alloc(std::max<long long>(c->m, 1)));
+  CUDA_TRY(c->q.alloc(c->n));
+  CUDA_TRY(c->jac.alloc(N));
+  CUDA_TRY(c->minv.alloc(N));
+  for (auto& b : c->x) CUDA_TRY(b.alloc(N));
+  CUDA_TRY(c->r.alloc(N));
+  CUDA_TRY(c->p.alloc(N));
+  CUDA_TRY(c->y.alloc(N));
+  CUDA_TRY(c->rhs.alloc(N));
+  CUDA_TRY(c->vin.alloc(N));
+  CUDA_TRY(c->zb.alloc(std::max<long long>(c->m, 1)));
+
+  c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 4, 1, 32);
+  // B'z strategy: atomic scatter by default; CSC when asked (deterministic)
+  c->scatter = (scatter == QPK_SCATTER_CSC) ? QPK_SCATTER_CSC : QPK_SCATTER_ATOMIC;
+  if (c->scatter == QPK_SCATTER_CSC) {
+    int rc = build_csc(c);
+    if (rc) return rc;
+  }
+
+  // grid sizes: persistent kernel = all co-resident blocks (capped by work)
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, pcg_kernel_for(c->lanes, c->scatter == QPK_SCATTER_CSC), QPK_BLOCK, 0));
+  if (per_sm < 1) return fail(QPK_E_UNSUPPORTED, "PCG kernel cannot be resident");
+  const long long work = std::max<long long>((long long)c->h_ci.size() / 1024, N / 512);
+  c->grid_pcg = (int)std::max<long long>(1, std::min<long long>((long long)per_sm * c->sms, work));
+  c->grid_std = c->grid_pcg;
+  CUDA_TRY(c->part.alloc((size_t)NSLOTS * c->grid_pcg));
+
+  Op o = c->op();
+  k_hdiag<<<std::max(1, std::min(c->sms * 4, (int)((c->n + 255) / 256))), 256, 0, s>>>(o.H, (int)c->n, c->hdiag.p);
+  c->launches++;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // host staging no longer needed
+  std::vector<int>().swap(c->h_ci);
+  std::vector<double>().swap(c->h_v);
+  std::vector<int>().swap(c->h_rp);
+  std::vector<double>().swap(c->h_dense);
+  std::vector<double>().swap(c->h_U);
+  std::vector<int>().swap(c->h_hci);
+  std::vector<double>().swap(c->h_hv);
+  c->building = false;
+  c->finalized = true;
+  return QPK_OK;
+}
+
+static int set_diagonals(qpk_ctx* c, const double* dd, const double* qq, cudaMemcpyKind kind) {
+  if (!c || !c->finalized) return fail(QPK_E_STATE, "qpk_set_diagonals: problem not finalized");
+  if ((c->m && !dd) || !qq) return fail(QPK_E_ARG, "qpk_set_diagonals: null vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->m) CUDA_TRY(cudaMemcpyAsync(c->d.p, dd, c->m * sizeof(double), kind, c->stream));
+  CUDA_TRY(cudaMemcpyAsync(c->q.p, qq, c->n * sizeof(double), kind, c->stream));
+  c->diag_set = true;
+  c->jac_ready = false;
+  return QPK_OK;
+}
+
+int qpk_set_diagonals(qpk_ctx* c, const double* dd, const double* qq) {
+  return set_diagonals(c, dd, qq, cudaMemcpyHostToDevice);
+}
+int qpk_set_diagonals_dev(qpk_ctx* c, const double* dd, const double* qq) {
+  return set_diagonals(c, dd, qq, cudaMemcpyDeviceToDevice);
+}
+
+static int build_jacobi(qpk_ctx* c) {
+  Op o = c->op();
+  const int G = c->grid_std;
+  cudaStream_t s = c->stream;
+  CUDA_TRY(cudaMemsetAsync(c->y.p, 0, c->n * sizeof(double), s));
+  if (c->m) {
+    if (c->have_csc) k_jac_cols<<<G, QPK_BLOCK, 0, s>>>(o, c->y.p);
+    else launch_jac_rows(c->lanes, G, s, o, c->y.p);
+    c->launches++;
+  }
+  k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
+  c->launches++;
+  CUDA_TRY(cudaGetLastError());
+  c->jac_ready = true;
+  return QPK_OK;
+}
+
+int qpk_jacobi(qpk_ctx* c, double* diag_out) {
+  if (!c || !c->diag_set) return fail(QPK_E_STATE, "qpk_jacobi: diagonals not set");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = build_jacobi(c);
+  if (rc) return rc;
+  if (diag_out) {
+    CUDA_TRY(cudaMemcpyAsync(diag_out, c->jac.p, c->N() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+static int apply_impl(qpk_ctx* c, const double* v_dev, double* y_dev) {
+  Op o = c->op();
+  const int G = c->grid_std;
+  cudaStream_t s = c->stream;
+  const bool csc = c->scatter == QPK_SCATTER_CSC;
+  k_prep<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev, c->part.p, G);
+  if (csc) launch_rows<true>(c->lanes, G, s, o, v_dev, y_dev, c->zb.p, c->part.p, G);
+  else launch_rows<false>(c->lanes, G, s, o, v_dev, y_dev, c->zb.p, c->part.p, G);
+  c->launches += 2;
+  if (csc) { k_finish_csc<<<G, QPK_BLOCK, 0, s>>>(o, y_dev, c->zb.p); c->launches++; }
+  CUDA_TRY(cudaGetLastError());
+  return QPK_OK;
+}
+
+int qpk_apply(qpk_ctx* c, const double* v, double* y) {
+  if (!c || !c->diag_set) return fail(QPK_E_STATE, "qpk_apply: diagonals not set");
+  if (!v || !y) return fail(QPK_E_ARG, "qpk_apply: null vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bytes = c->N() * sizeof(double);
+  CUDA_TRY(cudaMemcpyAsync(c->vin.p, v, bytes, cudaMemcpyHostToDevice, c->stream));
+  int rc = apply_impl(c, c->vin.p, c->y.p);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(y, c->y.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+int qpk_apply_dev(qpk_ctx* c, const double* v, double* y) {
+  if (!c || !c->diag_set) return fail(QPK_E_STATE, "qpk_apply_dev: diagonals not set");
+  if (!v || !y) return fail(QPK_E_ARG, "qpk_apply_dev: null vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  return apply_impl(c, v, y);
+}
+
+static int pcg_impl(qpk_ctx* c, const double* rhs_dev, double tol, int rel, int64_t max_iters, double* x_dev,
+                    qpk_pcg_info* info, double* hist_dev) {
+  if (!(tol > 0.0)) return fail(QPK_E_ARG, "tol must be positive");
+  if (max_iters < 1) return fail(QPK_E_ARG, "max_iters must be at least 1");
+  if (!c->jac_ready) { int rc = build_jacobi(c); if (rc) return rc; }
+  PcgParams P;
+  P.op = c->op();
+  P.rhs = rhs_dev;
+  P.x0 = c->x[0].p; P.x1 = c->x[1].p; P.x2 = c->x[2].p;
+  P.r = c->r.p; P.p = c->p.p; P.y = c->y.p; P.zb = c->zb.p; P.minv = c->minv.p;
+  P.part = c->part.p; P.G = c->grid_pcg;
+  P.tol = tol; P.rel = rel ? 1 : 0; P.max_iters = max_iters;
+  P.hist = hist_dev;
+  P.out = c->out.p;
+  void* args[] = {&P};
+  cudaEvent_t e0, e1;
+  CUDA_TRY(cudaEventCreate(&e0));
+  CUDA_TRY(cudaEventCreate(&e1));
+  CUDA_TRY(cudaEventRecord(e0, c->stream));
+  CUDA_TRY(cudaLaunchCooperativeKernel(pcg_kernel_for(c->lanes, c->scatter == QPK_SCATTER_CSC),
+                                       dim3(c->grid_pcg), dim3(QPK_BLOCK), args, 0, c->stream));
+  c->launches++;
+  CUDA_TRY(cudaEventRecord(e1, c->stream));
+  PcgOut o;
+  CUDA_TRY(cudaMemcpyAsync(&o, c->out.p, sizeof o, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  float ms = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double* res = c->x[o.result_buf].p;
+  CUDA_TRY(cudaMemcpyAsync(x_dev, res, c->N() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  if (info) {
+    info->iterations = o.iterations; info->converged = o.converged; info->status = o.status;
+    info->restarts = o.restarts; info->applies = o.applies; info->reserved = 0;
+    info->final_residual_norm = o.final_norm; info->threshold = o.threshold; info->rhs_norm = o.rhs_norm;
+    info->kernel_ms = ms;
+  }
+  return QPK_OK;
+}
+
+int qpk_pcg_dev(qpk_ctx* c, const double* rhs, double tol, int rel, int64_t max_iters, double* x,
+                qpk_pcg_info* info, double* hist) {
+  if (!c || !c->diag_set) return fail(QPK_E_STATE, "qpk_pcg_dev: diagonals not set");
+  if (!rhs || !x) return fail(QPK_E_ARG, "qpk_pcg_dev: null vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int rc = pcg_impl(c, rhs, tol, rel, max_iters, x, info, hist);
+  if (rc) return rc;
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+int qpk_pcg(qpk_ctx* c, const double* rhs, double tol, int rel, int64_t max_iters, double* x, qpk_pcg_info* info,
+            double* hist) {
+  if (!c || !c->diag_set) return fail(QPK_E_STATE, "qpk_pcg: diagonals not set");
+  if (!rhs || !x) return fail(QPK_E_ARG, "qpk_pcg: null vector");
+  if (max_iters < 1) return fail(QPK_E_ARG, "max_iters must be at least 1");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const size_t bytes = c->N() * sizeof(double);
+  CUDA_TRY(cudaMemcpyAsync(c->rhs.p, rhs, bytes, cudaMemcpyHostToDevice, c->stream));
+  double* hist_dev = nullptr;
+  if (hist) {
+    CUDA_TRY(c->hist.alloc(max_iters + 1));
+    hist_dev = c->hist.p;
+  }
+  int rc = pcg_impl(c, c->rhs.p, tol, rel, max_iters, c->vin.p, info, hist_dev);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(x, c->vin.p, bytes, cudaMemcpyDeviceToHost, c->stream));
+  if (hist) {
+    const long long cnt = (info ? info->iterations : max_iters) + 1;
+    CUDA_TRY(cudaMemcpyAsync(hist, hist_dev, std::min<long long>(cnt, max_iters + 1) * sizeof(double),
+                             cudaMemcpyDeviceToHost, c->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+int64_t qpk_query(qpk_ctx* c, const char* key) {
+  if (!c || !key) return -1;
+  std::string k(key);
+  if (k == "n") return c->n;
+  if (k == "m") return c->m;
+  if (k == "nnz") return c->nnz;
+  if (k == "nnz_padded") return (int64_t)(c->ci.n);
+  if (k == "lanes") return c->lanes;
+  if (k == "csc_lanes") return c->csc_lanes;
+  if (k == "scatter") return c->scatter;
+  if (k == "grid") return c->grid_pcg;
+  if (k == "block") return QPK_BLOCK;
+  if (k == "sms") return c->sms;
+  if (k == "hess_kind") return c->hkind;
+  if (k == "kernel_launches") return c->launches;
+  if (k == "device_bytes") {
+    size_t b = c->rp.bytes() + c->ci.bytes() + c->bv.bytes() + c->cp.bytes() + c->ri.bytes() + c->cv.bytes() +
+               c->hh.bytes() + c->hrp.bytes() + c->hci.bytes() + c->hv.bytes() + c->hdense.bytes() + c->U.bytes() +
+               c->w.bytes() + c->hdiag.bytes() + c->d.bytes() + c->q.bytes() + c->jac.bytes() + c->minv.bytes() +
+               c->r.bytes() + c->p.bytes() + c->y.bytes() + c->zb.bytes() + c->rhs.bytes() + c->part.bytes() +
+               c->vin.bytes() + c->hist.bytes();
+    for (auto& x : c->x) b += x.bytes();
+    return (int64_t)b;
+  }
+  return -1;
+}
+
+}  // extern "C"

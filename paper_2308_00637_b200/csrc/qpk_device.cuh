@@ -1,0 +1,286 @@
+// qpk_device.cuh -- device-side phases of the doubly augmented KKT operator
+// and of Jacobi-PCG, shared by the persistent cooperative solver kernel and
+// the standalone apply / Jacobi kernels (qpk.cu).
+//
+// Data layout in HBM:
+//   B      literal reference B = (C; A_l; -A_u) (kkt.py:177-184, 206-207),
+//          CSR with int32 columns, fp64 values, every row start padded to a
+//          multiple of 4 elements (padding: column -1, value 0) so a lane
+//          reads one int4 + two double2 per chunk of 4 nonzeros.
+//   B^T    optional CSC copy (int32 rows, fp64 values) for the deterministic,
+//          gather-only B'z pass.
+//   vectors of length N = n + m_B, top (n) first then bottom (m_B), exactly
+//          the reference's concatenation order (kkt.py:221).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define QPK_BLOCK 256
+#define QPK_KMAX 64
+
+namespace qpk {
+
+enum { HESS_DIAG = 0, HESS_CSR = 1, HESS_DENSE = 2, HESS_LOWRANK = 3 };
+
+struct Hess {
+  int kind;
+  const double* h;                      // DIAG: d ; LOWRANK: h0
+  const int* rp; const int* ci; const double* v; int lanes;  // CSR (full symmetric storage)
+  const double* dense;                  // n x n row-major
+  const double* U; const double* w; int k;                  // LOWRANK: U n x k row-major
+};
+
+struct Op {
+  int n, m;
+  const int* rp; const int* ci; const double* bv;           // padded CSR of B
+  const int* cp; const int* ri; const double* cv; int csc_lanes;  // CSC of B (may be null)
+  Hess H;
+  const double* d;                      // d_diag, m
+  const double* q;                      // q_diag_extra, n
+};
+
+// partial-sum slots (slot-major: part[slot * G + cta])
+enum { SLOT_ROWS = 0, SLOT_PREP = 1, SLOT_RR = 2, SLOT_RZ = 3, SLOT_AUX = 4, SLOT_S = 5,
+       NSLOTS = SLOT_S + QPK_KMAX };
+
+// ---------------------------------------------------------------- loads ----
+__device__ __forceinline__ int4 ld_stream_i4(const int* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+
+// ----------------------------------------------------------- reductions ----
+// Sum over the calling block; result broadcast to every thread.  Fixed tree:
+// deterministic for a fixed blockDim.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();                       // protect red[] from a previous use
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double t = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  return t;
+}
+
+// Sum of one partial slot over all G blocks, in a fixed order: every block
+// computes a bitwise identical value, so scalar control decisions (alpha,
+// beta, convergence, breakdown) agree across the grid without another sync.
+__device__ __forceinline__ double grid_total(const double* part, int G, double* red) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < G; i += blockDim.x) s += part[i];
+  return block_sum(s, red);
+}
+
+template <int L>
+__device__ __forceinline__ double subwarp_sum(double s) {
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// ------------------------------------------------------------ prep(v) ------
+// y_top = Q_diag-part * v (the part of Q u = H u + q_extra*u that is diagonal)
+// for element j, returns its contribution v_j * y_j to v'Kv.
+__device__ __forceinline__ double prep_elem(const Op& op, int j, double vj, double* y) {
+  const int kind = op.H.kind;
+  double qv = __dmul_rn(__ldg(op.q + j), vj);
+  double t;
+  if (kind == HESS_DIAG || kind == HESS_LOWRANK)
+    t = __dadd_rn(__dmul_rn(__ldg(op.H.h + j), vj), qv);     // hessian_apply + q*u (kkt.py:186-187)
+  else
+    t = qv;                                                 // H u added in the rows phase
+  y[j] = t;
+  return vj * t;
+}
+
+// accumulate the low-rank projection s = U' v over this thread's elements
+__device__ __forceinline__ void lowrank_accum(const Op& op, int j, double vj, double* sacc) {
+  const double* urow = op.H.U + (size_t)j * op.H.k;
+  for (int kk = 0; kk < op.H.k; ++kk) sacc[kk] += urow[kk] * vj;
+}
+
+__device__ __forceinline__ void lowrank_flush(const Op& op, double* sacc, double* part, int G, double* red) {
+  for (int kk = 0; kk < op.H.k; ++kk) {
+    double t = block_sum(sacc[kk], red);
+    if (threadIdx.x == 0) part[(SLOT_S + kk) * G + blockIdx.x] = t;
+  }
+}
+
+// prep phase over the top block: y_top = diag part of Q v; partial v'(diag Q)v
+__device__ void phase_prep(const Op& op, const double* v, double* y, double* part, int G, double* red) {
+  double acc = 0.0;
+  double sacc[QPK_KMAX];
+  const bool lr = op.H.kind == HESS_LOWRANK;
+  if (lr) for (int kk = 0; kk < op.H.k; ++kk) sacc[kk] = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < op.n; j += gridDim.x * blockDim.x) {
+    double vj = v[j];
+    acc += prep_elem(op, j, vj, y);
+    if (lr) lowrank_accum(op, j, vj, sacc);
+  }
+  double t = block_sum(acc, red);
+  if (threadIdx.x == 0) part[SLOT_PREP * G + blockIdx.x] = t;
+  if (lr) lowrank_flush(op, sacc, part, G, red);
+}
+
+// ------------------------------------------------------------ rows(v) ------
+// One pass over B: t = B u; z = 2 t / d + w; y_bottom = t + d w (kkt.py:217-220);
+// B' z either scattered with fp64 atomics into y_top (CSC == false) or z
+// stored for the gather pass (CSC == true).  Then the non-diagonal Hessian
+// part H u (CSR / dense / low-rank) is added to y_top.  Accumulates
+// t z + w y_bottom (+ u'H u) so that v'Kv is known after this phase:
+//   v'Kv = u'Q u + sum_r z_r t_r + sum_r w_r y_r   (since u'B'z = t'z).
+template <int L, bool CSC>
+__device__ void phase_rows(const Op& op, const double* __restrict__ v, double* y, double* zb,
+                           double* part, int G, double* red, double* s_lr) {
+  const double* u = v;
+  const double* w = v + op.n;
+  double acc = 0.0;
+  const int lane = threadIdx.x & (L - 1);
+  constexpr int RPW = 32 / L;                       // rows per warp step
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  const int sub_in_warp = (threadIdx.x & 31) / L;
+  for (long long rb = (long long)gwarp * RPW; rb < op.m; rb += (long long)nwarp * RPW) {
+    const int r = (int)rb + sub_in_warp;
+    const bool active = r < op.m;
+    int b = 0, e = 0;
+    if (active) { b = __ldg(op.rp + r); e = __ldg(op.rp + r + 1); }
+    const int k0 = b + 4 * lane;
+    int4 c0 = make_int4(-1, -1, -1, -1);
+    double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
+    if (k0 < e) { c0 = ld_stream_i4(op.ci + k0); v0 = ld_stream_d2(op.bv + k0); v1 = ld_stream_d2(op.bv + k0 + 2); }
+    double s = 0.0;
+    if (c0.x >= 0) s = fma(v0.x, u[c0.x], s);
+    if (c0.y >= 0) s = fma(v0.y, u[c0.y], s);
+    if (c0.z >= 0) s = fma(v1.x, u[c0.z], s);
+    if (c0.w >= 0) s = fma(v1.y, u[c0.w], s);
+    for (int k = k0 + 4 * L; k < e; k += 4 * L) {   // rows longer than 4L nonzeros
+      int4 c = ld_stream_i4(op.ci + k);
+      double2 a0 = ld_stream_d2(op.bv + k), a1 = ld_stream_d2(op.bv + k + 2);
+      if (c.x >= 0) s = fma(a0.x, u[c.x], s);
+      if (c.y >= 0) s = fma(a0.y, u[c.y], s);
+      if (c.z >= 0) s = fma(a1.x, u[c.z], s);
+      if (c.w >= 0) s = fma(a1.y, u[c.w], s);
+    }
+    const double t = subwarp_sum<L>(s);
+    if (!active) continue;
+    const double dr = __ldg(op.d + r), wr = w[r];
+    const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
+    const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
+    if (lane == 0) {
+      y[op.n + r] = yb;
+      acc += t * z + wr * yb;
+      if (CSC) zb[r] = z;
+    }
+    if (!CSC) {
+      if (c0.x >= 0) atomicAdd(y + c0.x, z * v0.x);
+      if (c0.y >= 0) atomicAdd(y + c0.y, z * v0.y);
+      if (c0.z >= 0) atomicAdd(y + c0.z, z * v1.x);
+      if (c0.w >= 0) atomicAdd(y + c0.w, z * v1.y);
+      for (int k = k0 + 4 * L; k < e; k += 4 * L) {
+        int4 c = *reinterpret_cast<const int4*>(op.ci + k);
+        double2 a0 = *reinterpret_cast<const double2*>(op.bv + k);
+        double2 a1 = *reinterpret_cast<const double2*>(op.bv + k + 2);
+        if (c.x >= 0) atomicAdd(y + c.x, z * a0.x);
+        if (c.y >= 0) atomicAdd(y + c.y, z * a0.y);
+        if (c.z >= 0) atomicAdd(y + c.z, z * a1.x);
+        if (c.w >= 0) atomicAdd(y + c.w, z * a1.y);
+      }
+    }
+  }
+
+  // non-diagonal Hessian part, added to y_top
+  const int kind = op.H.kind;
+  if (kind == HESS_CSR) {
+    const int LH = op.H.lanes;                       // power of two <= 32
+    const int lh = threadIdx.x & (LH - 1);
+    const int per = 32 / LH, sw = (threadIdx.x & 31) / LH;
+    for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
+      const int j = (int)jb + sw;
+      double s = 0.0;
+      if (j < op.n) {
+        const int b = __ldg(op.H.rp + j), e = __ldg(op.H.rp + j + 1);
+        for (int kk = b + lh; kk < e; kk += LH) s = fma(__ldg(op.H.v + kk), u[__ldg(op.H.ci + kk)], s);
+      }
+      for (int o = LH / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (j < op.n && lh == 0) { atomicAdd(y + j, s); acc += u[j] * s; }
+    }
+  } else if (kind == HESS_DENSE) {
+    const int ln = threadIdx.x & 31;
+    for (int j = gwarp; j < op.n; j += nwarp) {
+      const double* row = op.H.dense + (size_t)j * op.n;
+      double s = 0.0;
+      for (int c = ln; c < op.n; c += 32) s = fma(__ldg(row + c), u[c], s);
+      s = subwarp_sum<32>(s);
+      if (ln == 0) { atomicAdd(y + j, s); acc += u[j] * s; }
+    }
+  } else if (kind == HESS_LOWRANK) {
+    // s = U'u was accumulated in the prep phase; fold w in and apply U
+    const int k = op.H.k;
+    for (int kk = 0; kk < k; ++kk) {
+      double t = grid_total(part + (SLOT_S + kk) * G, G, red);
+      if (threadIdx.x == 0) s_lr[kk] = t;
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      double e2 = 0.0;
+      for (int kk = 0; kk < k; ++kk) e2 += op.H.w[kk] * s_lr[kk] * s_lr[kk];
+      acc += e2;                                      // u'U diag(w) U'u
+    }
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < op.n; j += gridDim.x * blockDim.x) {
+      const double* urow = op.H.U + (size_t)j * k;
+      double s = 0.0;
+      for (int kk = 0; kk < k; ++kk) s += urow[kk] * (op.H.w[kk] * s_lr[kk]);
+      atomicAdd(y + j, s);
+    }
+  }
+  double tot = block_sum(acc, red);
+  if (threadIdx.x == 0) part[SLOT_ROWS * G + blockIdx.x] = tot;
+}
+
+// CSC gather of (B'z)_j for column j by a group of LC lanes (all lanes get it)
+__device__ __forceinline__ double csc_col_sum(const Op& op, const double* zb, int j, bool valid, int lc, int LC) {
+  double s = 0.0;
+  if (valid) {
+    const int b = __ldg(op.cp + j), e = __ldg(op.cp + j + 1);
+    for (int k = b + lc; k < e; k += LC) s = fma(__ldg(op.cv + k), zb[__ldg(op.ri + k)], s);
+  }
+  for (int o = LC / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+// Visit every element i of the N-vector with its final K v value y_i.  In
+// CSC mode the top entries are completed here by the gather pass.  f(i, yi)
+// is called exactly once per element (by one lane).
+template <bool CSC, typename F>
+__device__ __forceinline__ void for_each_final(const Op& op, const double* y, const double* zb, F f) {
+  const int N = op.n + op.m;
+  if (!CSC) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) f(i, y[i]);
+    return;
+  }
+  const int LC = op.csc_lanes;
+  const int lc = threadIdx.x & (LC - 1);
+  const int per = 32 / LC, sw = (threadIdx.x & 31) / LC;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
+    const int j = (int)jb + sw;
+    const bool valid = j < op.n;
+    const double s = csc_col_sum(op, zb, j, valid, lc, LC);
+    if (valid && lc == 0) f(j, y[j] + s);
+  }
+  for (int i = op.n + blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) f(i, y[i]);
+}
+
+}  // namespace qpk

@@ -1,0 +1,181 @@
+"""Drop-in GPU direction solver for the reference IPM.
+
+``gpu_direction(op, rhs, cfg)`` has the signature of the reference hook
+``DirectionSolver = Callable[[KktOperator, np.ndarray, PcgConfig], PcgResult]``
+(qpipm/ipm.py:176) and the semantics of ``_pcg_direction`` (ipm.py:179-182):
+build the Jacobi diagonal, then run PCG from x0 = 0 on the doubly augmented
+operator.  It is passed as ``solve(problem, cfg, direction_solver=gpu_direction)``
+(ipm.py:185-187, called at ipm.py:206).
+
+* ``op`` is read by attribute: ``op.problem`` (n, a, c, hessian, m_eq),
+  ``op.bmap.lin_lower / lin_upper``, ``op.d_diag``, ``op.q_diag_extra``.  Both
+  the reference's KktOperator and ``problem.KktOperator`` work.
+* The problem data (B = (C; A_l; -A_u) and H) is uploaded once per problem
+  object and cached; only the two diagonals cross per IPM iteration.
+* Returns a ``PcgResult`` and raises ``PcgBreakdownError(result)`` on
+  nonpositive curvature -- the caller's own types when ``qpipm`` is loaded
+  (so the reference's ``except PcgBreakdownError`` at ipm.py:207 catches it),
+  otherwise this package's mirrors in ``pcg.py``.
+* There is no CPU fallback: without the CUDA library this raises.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import weakref
+
+import numpy as np
+
+from . import _native
+from .pcg import result_types
+
+
+class GpuKkt:
+    """Device-resident doubly augmented operator of one QpProblem."""
+
+    def __init__(self, problem, bmap, device: int = 0, scatter: int = _native.QPK_SCATTER_AUTO):
+        self.ctx = _native.Context(device)
+        self.n = int(problem.n)
+        lin_lower = np.ascontiguousarray(bmap.lin_lower, dtype=np.int64)
+        lin_upper = np.ascontiguousarray(bmap.lin_upper, dtype=np.int64)
+        m_e = int(problem.c.n_rows)
+        self.m = m_e + len(lin_lower) + len(lin_upper)
+        self.dim = self.n + self.m
+        c = self.ctx
+        c.call("qpk_problem_begin", self.n, m_e, len(lin_lower), len(lin_upper))
+        # B = (C; A_l; -A_u) in the reference's row order (kkt.py:177, 206-207)
+        cm = problem.c
+        if m_e:
+            ro, ci, v = _csr_arrays(cm)
+            c.call("qpk_problem_add_rows", int(cm.n_rows), _native.ptr(ro), _native.ptr(ci),
+                   _native.ptr(v), None, 0, 1.0)
+        am = problem.a
+        if len(lin_lower) or len(lin_upper):
+            ro, ci, v = _csr_arrays(am)
+            for rows, sign in ((lin_lower, 1.0), (lin_upper, -1.0)):
+                if len(rows):
+                    c.call("qpk_problem_add_rows", int(am.n_rows), _native.ptr(ro), _native.ptr(ci),
+                           _native.ptr(v), _native.ptr(rows), len(rows), sign)
+        self._set_hessian(problem.hessian)
+        if scatter == _native.QPK_SCATTER_AUTO:
+            scatter = int(os.environ.get("QPK_SCATTER", _native.QPK_SCATTER_ATOMIC))
+        c.call("qpk_problem_finalize", int(scatter))
+        self._hist = None
+
+    def _set_hessian(self, h):
+        kind = type(h).__name__
+        c = self.ctx
+        if kind == "DiagonalHessian":
+            d = np.ascontiguousarray(h.d, dtype=np.float64)
+            _dim(len(d), self.n, "Hessian")
+            c.call("qpk_set_hessian_diag", _native.ptr(d))
+        elif kind == "SparseHessian":
+            ro, ci, v = _csr_arrays(h.m)
+            _dim(h.m.n_rows, self.n, "Hessian")
+            c.call("qpk_set_hessian_csr", _native.ptr(ro), _native.ptr(ci), _native.ptr(v))
+        elif kind == "DenseHessian":
+            mm = np.ascontiguousarray(h.m, dtype=np.float64)
+            _dim(mm.shape[0], self.n, "Hessian")
+            c.call("qpk_set_hessian_dense", _native.ptr(mm))
+        elif kind == "QuasiNewtonHessian":
+            h0 = np.ascontiguousarray(h.h0_diag, dtype=np.float64)
+            u = np.ascontiguousarray(h.u, dtype=np.float64)
+            w = np.ascontiguousarray(h.w, dtype=np.float64)
+            _dim(len(h0), self.n, "Hessian")
+            c.call("qpk_set_hessian_lowrank", _native.ptr(h0), int(u.shape[1]), _native.ptr(u), _native.ptr(w))
+        else:
+            raise TypeError(f"unsupported Hessian type {kind}")
+
+    # -- per IPM iteration -------------------------------------------------
+    def set_diagonals(self, d_diag, q_extra):
+        d = np.ascontiguousarray(d_diag, dtype=np.float64)
+        q = np.ascontiguousarray(q_extra, dtype=np.float64)
+        _dim(len(d), self.m, "d_diag")
+        _dim(len(q), self.n, "q_diag_extra")
+        self.ctx.call("qpk_set_diagonals", _native.ptr(d), _native.ptr(q))
+
+    def jacobi(self) -> np.ndarray:
+        out = np.empty(self.dim)
+        self.ctx.call("qpk_jacobi", _native.ptr(out))
+        return out
+
+    def apply(self, v) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        _dim(len(v), self.dim, "vector")
+        y = np.empty(self.dim)
+        self.ctx.call("qpk_apply", _native.ptr(v), _native.ptr(y))
+        return y
+
+    def pcg(self, rhs, tol: float, max_iters: int, tol_is_relative: bool = True, history: bool = False):
+        """Returns (x, info, hist-or-None)."""
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        _dim(len(rhs), self.dim, "rhs")
+        x = np.empty(self.dim)
+        info = _native.PcgInfo()
+        hist = np.full(int(max_iters) + 1, np.nan) if history else None
+        self.ctx.call("qpk_pcg", _native.ptr(rhs), float(tol), int(bool(tol_is_relative)), int(max_iters),
+                      _native.ptr(x), _native.ctypes.byref(info), _native.ptr(hist) if history else None)
+        if history:
+            hist = hist[: info.iterations + 1]
+        return x, info, hist
+
+    def close(self):
+        self.ctx.close()
+
+
+def _dim(got, want, what):
+    if got != want:
+        from .problem import DimensionError
+        raise DimensionError(f"{what} has length {got}, expected {want}")
+
+
+def _csr_arrays(m):
+    return (np.ascontiguousarray(m.row_offsets, dtype=np.int64),
+            np.ascontiguousarray(m.col_indices, dtype=np.int64),
+            np.ascontiguousarray(m.values, dtype=np.float64))
+
+
+# one device copy per live problem object (the reference passes the same
+# QpProblem to every IPM iteration; kkt.py:372-377)
+_CACHE: "dict[int, tuple]" = {}
+
+
+def _finalizer(key):
+    entry = _CACHE.pop(key, None)
+    if entry is not None:
+        entry[1].close()
+
+
+def operator_for(op, device: int = 0) -> GpuKkt:
+    problem = op.problem
+    key = id(problem)
+    entry = _CACHE.get(key)
+    if entry is not None and entry[0]() is problem and entry[2] == _bmap_key(op.bmap):
+        return entry[1]
+    if entry is not None:
+        _finalizer(key)
+    gk = GpuKkt(problem, op.bmap, device=device)
+    try:
+        ref = weakref.ref(problem, lambda _r, k=key: _finalizer(k))
+    except TypeError:
+        ref = lambda p=problem: p  # noqa: E731  (unweakrefable problem: keep it alive)
+    _CACHE[key] = (ref, gk, _bmap_key(op.bmap))
+    return gk
+
+
+def _bmap_key(bmap):
+    return (len(bmap.lin_lower), len(bmap.lin_upper),
+            hash(np.asarray(bmap.lin_lower).tobytes()), hash(np.asarray(bmap.lin_upper).tobytes()))
+
+
+def gpu_direction(op, rhs, cfg):
+    """DirectionSolver: Jacobi-PCG on the GPU (ipm.py:179-182 semantics)."""
+    PcgResult, PcgBreakdownError = result_types()
+    gk = operator_for(op)
+    gk.set_diagonals(op.d_diag, op.q_diag_extra)
+    x, info, _ = gk.pcg(rhs, cfg.tol, cfg.max_iters, cfg.tol_is_relative)
+    result = PcgResult(x, int(info.iterations), float(info.final_residual_norm), bool(info.converged))
+    if info.status == _native.QPK_PCG_BREAKDOWN:
+        raise PcgBreakdownError(result)
+    return result

@@ -1,0 +1,20 @@
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device and the built libqpk.so")
+    config.addinivalue_line("markers", "slow: long-running")
+
+
+@pytest.fixture
+def rng():
+    return np.random.default_rng(20240817)
