@@ -145,6 +145,8 @@ def random_sweep(seed: int = 5, m: int = 4_000_000, n: int = 1_000_000, per_row:
     Draw order: column indices (rows with a repeated column are redrawn until
     none remain), values, h, log10 w, rhs.
     """
+    if per_row > n:
+        raise ValueError(f"cannot draw {per_row} distinct columns out of {n}")
     rng = np.random.default_rng(seed)
     cols = rng.integers(0, n, size=(m, per_row), dtype=np.int64)
     cols.sort(axis=1)
