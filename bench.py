@@ -205,13 +205,14 @@ def run_ours(args):
     assert info.iterations == args.iters and info.applies == args.iters + 1, (info.iterations, info.applies)
     barrier()
     launches0 = gk.ctx.query("kernel_launches")
-    kernel_ms = []
+    kernel_ms, phase_ms = [], []
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
             step()
             kernel_ms.append(info.kernel_ms)
+            phase_ms.append(list(info.phase_ms))
         ev1.record(stream)
         barrier()
     launches = gk.ctx.query("kernel_launches") - launches0
@@ -273,7 +274,9 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": per_launch, "algorithmic_bytes_per_iter": per_iter,
-                         "kernel": "pcg_kernel<4,false>", "kernel_ms_avg": avg_ms,
+                         "kernel": f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if args.scatter == 2 else 'false'}>", "kernel_ms_avg": avg_ms,
+                         "phase_us_per_iter": dict(zip(["direction_top", "rows_B_Bt", "residual_update", "other"],
+                                                       [round(v * 1e3 / args.iters, 2) for v in np.mean(phase_ms, axis=0)])),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "path": "gpu_direction(op, rhs, PcgConfig) host buffers"},

@@ -80,6 +80,10 @@ typedef struct {
   double threshold;            /* tol * ||rhs|| (relative) or tol */
   double rhs_norm;             /* ||rhs|| */
   double kernel_ms;            /* device time of the solve (CUDA events) */
+  double phase_ms[4];          /* time inside the solve kernel spent in the
+                                  direction/top phase, the rows (B, B') phase,
+                                  the residual-update phase, and the rest
+                                  (init, true residuals), from %globaltimer */
 } qpk_pcg_info;
 
 int qpk_abi_version(void);

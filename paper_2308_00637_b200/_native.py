@@ -14,7 +14,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libqpk.so"
+LIB_PATH = Path(os.environ.get("QPK_LIB", Path(__file__).resolve().parent / "libqpk.so"))
 
 QPK_OK = 0
 QPK_HESS_DIAG, QPK_HESS_CSR, QPK_HESS_DENSE, QPK_HESS_LOWRANK = 0, 1, 2, 3
@@ -47,6 +47,7 @@ class PcgInfo(ctypes.Structure):
         ("applies", ctypes.c_int32), ("reserved", ctypes.c_int32),
         ("final_residual_norm", ctypes.c_double), ("threshold", ctypes.c_double),
         ("rhs_norm", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+        ("phase_ms", ctypes.c_double * 4),
     ]
 
 

@@ -32,6 +32,20 @@ using namespace qpk;
 struct PcgOut {
   int iterations, converged, status, restarts, applies, result_buf;
   double final_norm, threshold, rhs_norm;
+  unsigned long long phase_ns[4];
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// per-phase wall time as seen by block 0 (includes waiting for the slowest block)
+struct PhaseClock {
+  unsigned long long last = 0, acc[4] = {0, 0, 0, 0};
+  __device__ void start() { last = globaltimer(); }
+  __device__ void lap(int phase) { const unsigned long long t = globaltimer(); acc[phase] += t - last; last = t; }
 };
 
 struct PcgParams {
@@ -48,33 +62,37 @@ struct PcgParams {
 
 __device__ __forceinline__ void write_out(const PcgParams& P, long long iters, int conv, int status,
                                           int restarts, int applies, int buf, double fin, double thr,
-                                          double rhs_norm) {
+                                          double rhs_norm, PhaseClock& pc) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
+    pc.lap(3);
+    for (int i = 0; i < 4; ++i) P.out->phase_ns[i] = pc.acc[i];
     P.out->iterations = (int)iters; P.out->converged = conv; P.out->status = status;
     P.out->restarts = restarts; P.out->applies = applies; P.out->result_buf = buf;
     P.out->final_norm = fin; P.out->threshold = thr; P.out->rhs_norm = rhs_norm;
   }
 }
 
-// p = z (+ beta p), z = minv * r ; then prep(p) for the next apply.
-// Partial sums: SLOT_AUX = r'z, SLOT_PREP = p'(diag Q)p, SLOT_S.. = U'p.
-__device__ void phase_direction(const PcgParams& P, double beta, bool restart, double* red) {
+// Top half of the direction update, with the lazy x update and the prep of
+// the next apply:  x_t <- x_t + alpha_prev p_t ;  z = minv r ;
+// p_t <- z (+ beta p_t) ;  y_t <- diag-part(Q) p_t.
+// Partial sums: SLOT_AUX = r'z (top), SLOT_PREP = p'(diag Q)p, SLOT_S.. = U'p.
+__device__ void phase_top(const PcgParams& P, const RowFuse& f, double* red) {
   const Op& op = P.op;
-  const int N = op.n + op.m, G = P.G;
+  const int G = P.G;
   double rz = 0.0, acc = 0.0;
   double sacc[QPK_KMAX];
   const bool lr = op.H.kind == HESS_LOWRANK;
   if (lr) for (int kk = 0; kk < op.H.k; ++kk) sacc[kk] = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    const double ri = P.r[i];
-    const double zi = __dmul_rn(__ldg(P.minv + i), ri);
-    rz += ri * zi;
-    const double pi = restart ? zi : __dadd_rn(zi, __dmul_rn(beta, P.p[i]));
-    P.p[i] = pi;
-    if (i < op.n) {
-      acc += prep_elem(op, i, pi, P.y);
-      if (lr) lowrank_accum(op, i, pi, sacc);
-    }
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < op.n; j += gridDim.x * blockDim.x) {
+    const double pold = P.p[j];
+    if (f.xupd) f.xdst[j] = __dadd_rn(f.xsrc[j], __dmul_rn(f.alpha_prev, pold));
+    const double rj = P.r[j];
+    const double zj = __dmul_rn(__ldg(P.minv + j), rj);
+    rz += rj * zj;
+    const double pn = f.restart ? zj : __dadd_rn(zj, __dmul_rn(f.beta, pold));
+    P.p[j] = pn;
+    acc += prep_elem(op, j, pn, P.y);
+    if (lr) lowrank_accum(op, j, pn, sacc);
   }
   double t = block_sum(rz, red);
   if (threadIdx.x == 0) P.part[SLOT_AUX * G + blockIdx.x] = t;
@@ -83,8 +101,78 @@ __device__ void phase_direction(const PcgParams& P, double beta, bool restart, d
   if (lr) lowrank_flush(op, sacc, P.part, G, red);
 }
 
+// r <- r - alpha y ; partial r'r and r'z (z = minv r).  Atomic mode: y is final,
+// vectorised over pairs; CSC mode: top entries of y completed by the gather.
+template <bool CSC>
+__device__ void phase_update(const PcgParams& P, double alpha, double* red) {
+  const Op& op = P.op;
+  const int N = op.n + op.m, G = P.G;
+  double rr = 0.0, rz = 0.0;
+  if (!CSC) {
+    const int np = N >> 1;
+    double2* r2 = reinterpret_cast<double2*>(P.r);
+    const double2* y2 = reinterpret_cast<const double2*>(P.y);
+    const double2* m2 = reinterpret_cast<const double2*>(P.minv);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+      double2 ri = r2[i];
+      const double2 yi = y2[i];
+      const double2 mi = __ldg(m2 + i);
+      ri.x = __dsub_rn(ri.x, __dmul_rn(alpha, yi.x));
+      ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yi.y));
+      r2[i] = ri;
+      rr += ri.x * ri.x + ri.y * ri.y;
+      rz += ri.x * __dmul_rn(mi.x, ri.x) + ri.y * __dmul_rn(mi.y, ri.y);
+    }
+    if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      const int i = N - 1;
+      const double ri = __dsub_rn(P.r[i], __dmul_rn(alpha, P.y[i]));
+      P.r[i] = ri;
+      rr += ri * ri;
+      rz += ri * __dmul_rn(__ldg(P.minv + i), ri);
+    }
+  } else {
+    for_each_final<true>(op, P.y, P.zb, [&](int i, double yi) {
+      const double ri = __dsub_rn(P.r[i], __dmul_rn(alpha, yi));
+      P.r[i] = ri;
+      rr += ri * ri;
+      rz += ri * __dmul_rn(__ldg(P.minv + i), ri);
+    });
+  }
+  double t = block_sum(rr, red);
+  if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
+  t = block_sum(rz, red);
+  if (threadIdx.x == 0) P.part[SLOT_RZ * G + blockIdx.x] = t;
+}
+
+__device__ __forceinline__ int spare_buffer(int cur, int best) {
+  return (cur != best) ? 3 - cur - best : (cur + 1) % 3;
+}
+
+// explicit residual r = rhs - K x (linalg.py:113-114, 132); partial ||r||^2 -> SLOT_RR
 template <int L, bool CSC>
-__global__ void __launch_bounds__(QPK_BLOCK) pcg_kernel(PcgParams P) {
+__device__ double true_residual(const PcgParams& P, double* x, bool store_r, double* red, double* s_lr) {
+  cg::grid_group grid = cg::this_grid();
+  const Op& op = P.op;
+  const int G = P.G;
+  phase_prep(op, x, P.y, P.part, G, red);
+  grid.sync();
+  RowFuse none{};
+  phase_rows<L, CSC, false>(op, x, P.y, P.zb, P.part, G, red, s_lr, none);
+  grid.sync();
+  double rr = 0.0;
+  for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
+    const double ri = __dsub_rn(__ldg(P.rhs + i), yi);
+    if (store_r) P.r[i] = ri;
+    rr += ri * ri;
+  });
+  const double t = block_sum(rr, red);
+  if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
+  grid.sync();
+  return sqrt(grid_total(P.part + SLOT_RR * G, G, red));
+}
+
+template <int L, bool CSC>
+__global__ void __launch_bounds__(QPK_BLOCK, QPK_PCG_MIN_BLOCKS) pcg_kernel(PcgParams P) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double red[32];
   __shared__ double s_lr[QPK_KMAX];
@@ -92,6 +180,8 @@ __global__ void __launch_bounds__(QPK_BLOCK) pcg_kernel(PcgParams P) {
   const int N = op.n + op.m, G = P.G;
   double* xs[3] = {P.x0, P.x1, P.x2};
   const bool writer = blockIdx.x == 0 && threadIdx.x == 0;
+  PhaseClock pc;
+  if (writer) pc.start();
 
   // x = 0, r = rhs (linalg.py:85-87), ||rhs||
   {
@@ -109,107 +199,86 @@ __global__ void __launch_bounds__(QPK_BLOCK) pcg_kernel(PcgParams P) {
   const double rhs_norm = sqrt(grid_total(P.part + SLOT_AUX * G, G, red));
   const double thr = P.rel ? P.tol * rhs_norm : P.tol;          // linalg.py:83
   double rnorm = rhs_norm, best_rnorm = rhs_norm;
-  int cur = 0, best = 0, restarts = 0, applies = 0;
+  int cur = 0, best = 0, xn = 0, restarts = 0, applies = 0;
   if (writer && P.hist) P.hist[0] = rnorm;
   if (rnorm <= thr) {                                               // linalg.py:93-94
-    write_out(P, 0, 1, QPK_PCG_OK, 0, 0, 0, rnorm, thr, rhs_norm);
+    write_out(P, 0, 1, QPK_PCG_OK, 0, 0, 0, rnorm, thr, rhs_norm, pc);
     return;
   }
-  phase_direction(P, 0.0, true, red);                               // z, p = z, r'z
-  grid.sync();
-  double rz = grid_total(P.part + SLOT_AUX * G, G, red);
+  // f carries the pending state: restart (p = z), beta, lazy x update
+  RowFuse f{};
+  f.r = P.r;
+  f.restart = 1;
+  f.xupd = 0;
+  double rz = 0.0;
 
   for (long long k = 1; k <= P.max_iters; ++k) {
-    // y = K p  (+ p'Kp)
-    phase_rows<L, CSC>(op, P.p, P.y, P.zb, P.part, G, red, s_lr);
+    f.xsrc = xs[cur];
+    f.xdst = xs[xn];
+    // p <- z (+ beta p) and x <- x + alpha p (top half), y_top init
+    phase_top(P, f, red);
+    grid.sync();
+    if (writer) pc.lap(0);
+    // y = K p; bottom half of the direction/x update fused in
+    phase_rows<L, CSC, true>(op, P.p, P.y, P.zb, P.part, G, red, s_lr, f);
     ++applies;
     grid.sync();
+    if (writer) pc.lap(1);
+    if (f.xupd) { cur = xn; f.xupd = 0; }
+    if (f.restart) rz = grid_total(P.part + SLOT_AUX * G, G, red) + grid_total(P.part + SLOT_AUX2 * G, G, red);
     const double pap = grid_total(P.part + SLOT_ROWS * G, G, red) + grid_total(P.part + SLOT_PREP * G, G, red);
     if (pap <= 0.0) {                                               // linalg.py:102-103
-      write_out(P, k - 1, 0, QPK_PCG_BREAKDOWN, restarts, applies, best, best_rnorm, thr, rhs_norm);
+      write_out(P, k - 1, 0, QPK_PCG_BREAKDOWN, restarts, applies, best, best_rnorm, thr, rhs_norm, pc);
       return;
     }
     const double alpha = rz / pap;
-    const int xn = (cur != best) ? 3 - cur - best : (cur + 1) % 3;
-    {
-      const double* xc = xs[cur];
-      double* xw = xs[xn];
-      double rr = 0.0, rzn = 0.0;
-      for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
-        xw[i] = __dadd_rn(xc[i], __dmul_rn(alpha, P.p[i]));       // x += alpha p
-        const double ri = __dsub_rn(P.r[i], __dmul_rn(alpha, yi));  // r -= alpha op_p
-        P.r[i] = ri;
-        const double zi = __dmul_rn(__ldg(P.minv + i), ri);
-        rr += ri * ri;
-        rzn += ri * zi;
-      });
-      double t = block_sum(rr, red);
-      if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
-      t = block_sum(rzn, red);
-      if (threadIdx.x == 0) P.part[SLOT_RZ * G + blockIdx.x] = t;
-    }
+    phase_update<CSC>(P, alpha, red);                               // r -= alpha y
     grid.sync();
-    cur = xn;
+    if (writer) pc.lap(2);
     rnorm = sqrt(grid_total(P.part + SLOT_RR * G, G, red));
     if (writer && P.hist) P.hist[k] = rnorm;
-    if (rnorm < best_rnorm) { best = cur; best_rnorm = rnorm; }     // linalg.py:110-111
+    // x_k = x_{k-1} + alpha p is pending; it will land in buffer xn
+    xn = spare_buffer(cur, best);
+    f.xupd = 1;
+    f.alpha_prev = alpha;
+    if (rnorm < best_rnorm) { best = xn; best_rnorm = rnorm; }      // linalg.py:110-111
     if (rnorm <= thr) {
-      // explicit residual rhs - K x (linalg.py:112-116)
-      phase_prep(op, xs[cur], P.y, P.part, G, red);
+      // materialise x_k, then the explicit residual (linalg.py:112-116)
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+        xs[xn][i] = __dadd_rn(xs[cur][i], __dmul_rn(alpha, P.p[i]));
       grid.sync();
-      phase_rows<L, CSC>(op, xs[cur], P.y, P.zb, P.part, G, red, s_lr);
+      cur = xn;
+      f.xupd = 0;
+      const double true_norm = true_residual<L, CSC>(P, xs[cur], true, red, s_lr);
       ++applies;
-      grid.sync();
-      {
-        double rr = 0.0;
-        for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
-          const double ri = __dsub_rn(__ldg(P.rhs + i), yi);
-          P.r[i] = ri;
-          rr += ri * ri;
-        });
-        const double t = block_sum(rr, red);
-        if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
-      }
-      grid.sync();
-      const double true_norm = sqrt(grid_total(P.part + SLOT_RR * G, G, red));
       if (true_norm <= thr) {
-        write_out(P, k, 1, QPK_PCG_OK, restarts, applies, cur, true_norm, thr, rhs_norm);
+        write_out(P, k, 1, QPK_PCG_OK, restarts, applies, cur, true_norm, thr, rhs_norm, pc);
         return;
       }
       // recurrence drifted: restart from the explicit residual (linalg.py:117-125)
       ++restarts;
       rnorm = true_norm;
       if (rnorm < best_rnorm) { best = cur; best_rnorm = rnorm; }
-      phase_direction(P, 0.0, true, red);
-      grid.sync();
-      rz = grid_total(P.part + SLOT_AUX * G, G, red);
+      f.restart = 1;
       continue;
     }
     const double rz_next = grid_total(P.part + SLOT_RZ * G, G, red);  // linalg.py:126-130
-    const double beta = rz_next / rz;
+    f.beta = rz_next / rz;
+    f.restart = 0;
     rz = rz_next;
-    phase_direction(P, beta, false, red);
+  }
+  // iteration cap: materialise the pending iterate, then the true residual of
+  // the best one (linalg.py:132-133)
+  if (f.xupd) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+      xs[xn][i] = __dadd_rn(xs[cur][i], __dmul_rn(f.alpha_prev, P.p[i]));
     grid.sync();
+    cur = xn;
   }
-  // iteration cap: true residual of the best iterate (linalg.py:132-133)
-  phase_prep(op, xs[best], P.y, P.part, G, red);
-  grid.sync();
-  phase_rows<L, CSC>(op, xs[best], P.y, P.zb, P.part, G, red, s_lr);
+  const double true_norm = true_residual<L, CSC>(P, xs[best], false, red, s_lr);
   ++applies;
-  grid.sync();
-  {
-    double rr = 0.0;
-    for_each_final<CSC>(op, P.y, P.zb, [&](int i, double yi) {
-      const double ri = __dsub_rn(__ldg(P.rhs + i), yi);
-      rr += ri * ri;
-    });
-    const double t = block_sum(rr, red);
-    if (threadIdx.x == 0) P.part[SLOT_RR * G + blockIdx.x] = t;
-  }
-  grid.sync();
-  const double true_norm = sqrt(grid_total(P.part + SLOT_RR * G, G, red));
   write_out(P, P.max_iters, true_norm <= thr ? 1 : 0, QPK_PCG_OK, restarts, applies, best, true_norm, thr,
-            rhs_norm);
+            rhs_norm, pc);
 }
 
 // ---------------------------------------------------- standalone phases ---
@@ -222,7 +291,8 @@ template <int L, bool CSC>
 __global__ void __launch_bounds__(QPK_BLOCK) k_rows(Op op, const double* v, double* y, double* zb, double* part, int G) {
   __shared__ double red[32];
   __shared__ double s_lr[QPK_KMAX];
-  phase_rows<L, CSC>(op, v, y, zb, part, G, red, s_lr);
+  RowFuse none{};
+  phase_rows<L, CSC, false>(op, const_cast<double*>(v), y, zb, part, G, red, s_lr, none);
 }
 
 __global__ void __launch_bounds__(QPK_BLOCK) k_finish_csc(Op op, double* y, const double* zb) {
@@ -258,9 +328,13 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_jac_cols(Op op, double* acc) {
     double s = 0.0;
     if (j < op.n) {
       const int b = __ldg(op.cp + j), e = __ldg(op.cp + j + 1);
-      for (int k = b + lc; k < e; k += LC) {
-        const double a = __ldg(op.cv + k);
-        s += __dmul_rn(a, a) * (1.0 / __ldg(op.d + __ldg(op.ri + k)));
+      for (int k = b + 4 * lc; k < e; k += 4 * LC) {
+        const int4 c = ld_stream_i4(op.ri + k);
+        const double2 a0 = ld_stream_d2(op.cv + k), a1 = ld_stream_d2(op.cv + k + 2);
+        if (c.x >= 0) s += __dmul_rn(a0.x, a0.x) * (1.0 / __ldg(op.d + c.x));
+        if (c.y >= 0) s += __dmul_rn(a0.y, a0.y) * (1.0 / __ldg(op.d + c.y));
+        if (c.z >= 0) s += __dmul_rn(a1.x, a1.x) * (1.0 / __ldg(op.d + c.z));
+        if (c.w >= 0) s += __dmul_rn(a1.y, a1.y) * (1.0 / __ldg(op.d + c.w));
       }
     }
     for (int o = LC / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -577,13 +651,22 @@ int qpk_set_hessian_lowrank(qpk_ctx* c, const double* h0, int64_t k, const doubl
   return QPK_OK;
 }
 
+// B' as CSC, every column padded to a multiple of 4 entries (row -1, value 0);
+// rows inside a column ascend (deterministic gather order)
 static int build_csc(qpk_ctx* c) {
   const long long n = c->n;
+  std::vector<long long> cnt(n, 0);
+  for (int col : c->h_ci) if (col >= 0) cnt[col]++;
   std::vector<int> cp(n + 1, 0);
-  for (int col : c->h_ci) if (col >= 0) cp[col + 1]++;
-  for (long long j = 0; j < n; ++j) cp[j + 1] += cp[j];
-  std::vector<int> ri(c->nnz);
-  std::vector<double> cv(c->nnz);
+  long long tot = 0;
+  for (long long j = 0; j < n; ++j) {
+    cp[j] = (int)tot;
+    tot += (cnt[j] + 3) & ~3LL;
+    if (tot >= (1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "padded CSC exceeds int32 range");
+  }
+  cp[n] = (int)tot;
+  std::vector<int> ri(tot, -1);
+  std::vector<double> cv(tot, 0.0);
   std::vector<int> pos(cp.begin(), cp.end() - 1);
   for (long long r = 0; r < c->m; ++r)
     for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
@@ -597,7 +680,8 @@ static int build_csc(qpk_ctx* c) {
   CUDA_TRY(upload(c->ri, ri, c->stream));
   CUDA_TRY(upload(c->cv, cv, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
-  c->csc_lanes = pow2_clamp((c->nnz + n - 1) / std::max<long long>(n, 1) / 2, 1, 32);
+  // lanes per column: ~16 entries (4 chunks) per lane
+  c->csc_lanes = pow2_clamp((tot / std::max<long long>(n, 1) + 15) / 16, 1, 32);
   c->have_csc = true;
   return QPK_OK;
 }
@@ -791,6 +875,7 @@ static int pcg_impl(qpk_ctx* c, const double* rhs_dev, double tol, int rel, int6
     info->restarts = o.restarts; info->applies = o.applies; info->reserved = 0;
     info->final_residual_norm = o.final_norm; info->threshold = o.threshold; info->rhs_norm = o.rhs_norm;
     info->kernel_ms = ms;
+    for (int i = 0; i < 4; ++i) info->phase_ms[i] = o.phase_ns[i] * 1e-6;
   }
   return QPK_OK;
 }

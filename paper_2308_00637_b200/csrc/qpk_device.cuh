@@ -17,6 +17,9 @@
 
 #define QPK_BLOCK 256
 #define QPK_KMAX 64
+#ifndef QPK_PCG_MIN_BLOCKS
+#define QPK_PCG_MIN_BLOCKS 4
+#endif
 
 namespace qpk {
 
@@ -40,7 +43,7 @@ struct Op {
 };
 
 // partial-sum slots (slot-major: part[slot * G + cta])
-enum { SLOT_ROWS = 0, SLOT_PREP = 1, SLOT_RR = 2, SLOT_RZ = 3, SLOT_AUX = 4, SLOT_S = 5,
+enum { SLOT_ROWS = 0, SLOT_PREP = 1, SLOT_RR = 2, SLOT_RZ = 3, SLOT_AUX = 4, SLOT_AUX2 = 5, SLOT_S = 6,
        NSLOTS = SLOT_S + QPK_KMAX };
 
 // ---------------------------------------------------------------- loads ----
@@ -133,18 +136,30 @@ __device__ void phase_prep(const Op& op, const double* v, double* y, double* par
 }
 
 // ------------------------------------------------------------ rows(v) ------
+// Bottom-half work of the PCG direction update, fused into the rows pass
+// (which is bound by random L2 requests, so this streaming is nearly free):
+//   x_b <- x_b + alpha_prev p_b      (lazy x update of the previous iteration)
+//   p_b <- (1/d) r_b (+ beta p_b)    (z = M^-1 r with M_bottom = D, linalg.py:126-130)
+struct RowFuse {
+  const double* r;
+  const double* xsrc;
+  double* xdst;
+  double alpha_prev, beta;
+  int restart, xupd;
+};
+
 // One pass over B: t = B u; z = 2 t / d + w; y_bottom = t + d w (kkt.py:217-220);
 // B' z either scattered with fp64 atomics into y_top (CSC == false) or z
 // stored for the gather pass (CSC == true).  Then the non-diagonal Hessian
 // part H u (CSR / dense / low-rank) is added to y_top.  Accumulates
 // t z + w y_bottom (+ u'H u) so that v'Kv is known after this phase:
 //   v'Kv = u'Q u + sum_r z_r t_r + sum_r w_r y_r   (since u'B'z = t'z).
-template <int L, bool CSC>
-__device__ void phase_rows(const Op& op, const double* __restrict__ v, double* y, double* zb,
-                           double* part, int G, double* red, double* s_lr) {
+template <int L, bool CSC, bool FUSE>
+__device__ void phase_rows(const Op& op, double* v, double* y, double* zb,
+                           double* part, int G, double* red, double* s_lr, const RowFuse& f) {
   const double* u = v;
-  const double* w = v + op.n;
-  double acc = 0.0;
+  double* w = v + op.n;
+  double acc = 0.0, rzb = 0.0;
   const int lane = threadIdx.x & (L - 1);
   constexpr int RPW = 32 / L;                       // rows per warp step
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -154,7 +169,21 @@ __device__ void phase_rows(const Op& op, const double* __restrict__ v, double* y
     const int r = (int)rb + sub_in_warp;
     const bool active = r < op.m;
     int b = 0, e = 0;
-    if (active) { b = __ldg(op.rp + r); e = __ldg(op.rp + r + 1); }
+    double dr = 1.0, wr = 0.0;
+    if (active) {
+      b = __ldg(op.rp + r); e = __ldg(op.rp + r + 1);
+      dr = __ldg(op.d + r);
+      wr = w[r];
+      if (FUSE) {
+        // every lane of the row computes the same values; lane 0 stores
+        const double rr = f.r[op.n + r];
+        const double zr = __dmul_rn(1.0 / dr, rr);
+        if (f.xupd && lane == 0) f.xdst[op.n + r] = __dadd_rn(f.xsrc[op.n + r], __dmul_rn(f.alpha_prev, wr));
+        const double pn = f.restart ? zr : __dadd_rn(zr, __dmul_rn(f.beta, wr));
+        if (lane == 0) { w[r] = pn; rzb += rr * zr; }
+        wr = pn;
+      }
+    }
     const int k0 = b + 4 * lane;
     int4 c0 = make_int4(-1, -1, -1, -1);
     double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
@@ -174,7 +203,6 @@ __device__ void phase_rows(const Op& op, const double* __restrict__ v, double* y
     }
     const double t = subwarp_sum<L>(s);
     if (!active) continue;
-    const double dr = __ldg(op.d + r), wr = w[r];
     const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
     const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
     if (lane == 0) {
@@ -197,6 +225,10 @@ __device__ void phase_rows(const Op& op, const double* __restrict__ v, double* y
         if (c.w >= 0) atomicAdd(y + c.w, z * a1.y);
       }
     }
+  }
+  if (FUSE) {
+    const double t2 = block_sum(rzb, red);
+    if (threadIdx.x == 0) part[SLOT_AUX2 * G + blockIdx.x] = t2;
   }
 
   // non-diagonal Hessian part, added to y_top
@@ -248,13 +280,38 @@ __device__ void phase_rows(const Op& op, const double* __restrict__ v, double* y
   if (threadIdx.x == 0) part[SLOT_ROWS * G + blockIdx.x] = tot;
 }
 
-// CSC gather of (B'z)_j for column j by a group of LC lanes (all lanes get it)
+// CSC gather of (B'z)_j for column j by a group of LC lanes (all lanes get
+// the sum).  Columns are padded to multiples of 4 entries (row index -1), so a
+// lane reads one int4 of row indices + two double2 of values per chunk and has
+// 4 independent z gathers in flight per chunk (two chunks per loop trip).
 __device__ __forceinline__ double csc_col_sum(const Op& op, const double* zb, int j, bool valid, int lc, int LC) {
-  double s = 0.0;
+  double s0 = 0.0, s1 = 0.0;
   if (valid) {
     const int b = __ldg(op.cp + j), e = __ldg(op.cp + j + 1);
-    for (int k = b + lc; k < e; k += LC) s = fma(__ldg(op.cv + k), zb[__ldg(op.ri + k)], s);
+    int k = b + 4 * lc;
+    for (; k + 4 * LC < e; k += 8 * LC) {
+      const int4 c = ld_stream_i4(op.ri + k), d = ld_stream_i4(op.ri + k + 4 * LC);
+      const double2 a0 = ld_stream_d2(op.cv + k), a1 = ld_stream_d2(op.cv + k + 2);
+      const double2 b0 = ld_stream_d2(op.cv + k + 4 * LC), b1 = ld_stream_d2(op.cv + k + 4 * LC + 2);
+      if (c.x >= 0) s0 = fma(a0.x, zb[c.x], s0);
+      if (c.y >= 0) s0 = fma(a0.y, zb[c.y], s0);
+      if (c.z >= 0) s0 = fma(a1.x, zb[c.z], s0);
+      if (c.w >= 0) s0 = fma(a1.y, zb[c.w], s0);
+      if (d.x >= 0) s1 = fma(b0.x, zb[d.x], s1);
+      if (d.y >= 0) s1 = fma(b0.y, zb[d.y], s1);
+      if (d.z >= 0) s1 = fma(b1.x, zb[d.z], s1);
+      if (d.w >= 0) s1 = fma(b1.y, zb[d.w], s1);
+    }
+    if (k < e) {
+      const int4 c = ld_stream_i4(op.ri + k);
+      const double2 a0 = ld_stream_d2(op.cv + k), a1 = ld_stream_d2(op.cv + k + 2);
+      if (c.x >= 0) s0 = fma(a0.x, zb[c.x], s0);
+      if (c.y >= 0) s0 = fma(a0.y, zb[c.y], s0);
+      if (c.z >= 0) s0 = fma(a1.x, zb[c.z], s0);
+      if (c.w >= 0) s0 = fma(a1.y, zb[c.w], s0);
+    }
   }
+  double s = s0 + s1;
   for (int o = LC / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
 }
@@ -277,8 +334,9 @@ __device__ __forceinline__ void for_each_final(const Op& op, const double* y, co
   for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
     const int j = (int)jb + sw;
     const bool valid = j < op.n;
+    const double yj = valid ? y[j] : 0.0;
     const double s = csc_col_sum(op, zb, j, valid, lc, LC);
-    if (valid && lc == 0) f(j, y[j] + s);
+    if (valid && lc == 0) f(j, yj + s);
   }
   for (int i = op.n + blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) f(i, y[i]);
 }
