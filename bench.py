@@ -51,7 +51,12 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=10, help="oracle iterations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters-per-step", type=int, default=5)
-    return ap.parse_args()
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg5 = headline sweep; cfg1-4 = PCG sweep on the first IPM iteration's operator")
+    args = ap.parse_args()
+    if args.workload != "cfg5" and args.iters == 500:
+        args.iters = 200
+    return args
 
 
 def dist_env():
@@ -61,22 +66,66 @@ def dist_env():
     return rank, world, local
 
 
-def make_workload(scale: float, seed: int = 5):
+WORKLOAD_DESC = {
+    "cfg1": "cfg1 dense QP n=200, m=400 (DenseHessian Q'Q+1e-2 I)",
+    "cfg2": "cfg2 SVM primal d=500, N=50,000 (A = [diag(y)X, y, I], 502 nnz/row)",
+    "cfg3": "cfg3 RT-like 200,000 voxels x 20,000 beamlets, 0.5% band density, SparseHessian D_t'D_t",
+    "cfg4": "cfg4 RT-like 2,000,000 voxels x 100,000 beamlets, 0.1% band density, SparseHessian D_t'D_t",
+    "cfg5": "cfg5 operator sweep 4,000,000 x 1,000,000, 16 nnz/row, H=diag(U(1e-2,1)), log10 w ~ U(-6,6)",
+}
+
+
+def make_workload(name: str, scale: float, seed_offset: int = 0):
+    """(problem, op, rhs, meta).  cfg5: the BASELINE sweep with its seeded rhs;
+    cfg1-4: the operator of the first IPM iteration with a seeded N(0,1) rhs."""
     from paper_2308_00637_b200 import workloads
     from paper_2308_00637_b200.problem import build_operator
-    m, n = int(4_000_000 * scale), int(1_000_000 * scale)
-    problem, state, meta = workloads.random_sweep(seed=seed, m=m, n=n)
+    if name == "cfg5":
+        m, n = int(4_000_000 * scale), int(1_000_000 * scale)
+        problem, state, meta = workloads.random_sweep(seed=5 + seed_offset, m=m, n=n)
+        rhs = meta.pop("rhs")
+    else:
+        if name == "cfg1":
+            problem, state, meta = workloads.dense_qp(seed=0 + seed_offset)
+        elif name == "cfg2":
+            problem, state, meta = workloads.svm_primal(seed=2 + seed_offset, n_samples=int(50_000 * scale))
+        elif name == "cfg3":
+            problem, state, meta = workloads.rt_like(seed=3 + seed_offset, n_vox=int(200_000 * scale),
+                                                     n_beam=int(20_000 * scale))
+        else:
+            problem, state, meta = workloads.rt_like(seed=4 + seed_offset, n_vox=int(2_000_000 * scale),
+                                                     n_beam=int(100_000 * scale), density=0.001)
+        rhs = np.random.default_rng(77 + seed_offset).standard_normal(problem.n + len(state.s_lA) + len(state.s_uA)
+                                                                      + problem.m_eq)
     op = build_operator(problem, state)
-    return problem, op, meta
+    assert len(rhs) == op.dim
+    return problem, op, rhs, meta
 
 
 def algorithmic_bytes(op, iters: int, applies: int):
-    """SURVEY.md 8(d): bytes_B = 12 nnz + 4 (m_B + 1); diagonal H adds 0;
-    per PCG iteration bytes_B + 88 N; per extra apply bytes_B + 24 N."""
-    nnz = op.problem.a.nnz
+    """SURVEY.md 8(d): bytes_B = 12 nnz_B + 4 (m_B + 1) (two-sided rows once);
+    bytes_Hm = 0 (diagonal), 12 nnz_H + 4 (n + 1) (sparse), 8 n^2 (dense),
+    16 n k + 8 k (low rank); per PCG iteration bytes_B + bytes_Hm + 88 N; per
+    extra apply bytes_B + bytes_Hm + 24 N.  Returns (per launch, per iteration)."""
+    p = op.problem
+    rows = set(np.asarray(op.bmap.lin_lower).tolist()) | set(np.asarray(op.bmap.lin_upper).tolist())
+    lens = np.diff(p.a.row_offsets)
+    nnz = int(lens[sorted(rows)].sum()) if rows else 0
+    nnz += p.c.nnz
     N = op.dim
     bytes_b = 12 * nnz + 4 * (op.m + 1)
-    return iters * (bytes_b + 88 * N) + applies * (bytes_b + 24 * N), bytes_b + 88 * N
+    h = p.hessian
+    kind = type(h).__name__
+    if kind == "SparseHessian":
+        bytes_h = 12 * h.m.nnz + 4 * (p.n + 1)
+    elif kind == "DenseHessian":
+        bytes_h = 8 * p.n * p.n
+    elif kind == "QuasiNewtonHessian":
+        bytes_h = 16 * p.n * h.u.shape[1] + 8 * h.u.shape[1]
+    else:
+        bytes_h = 0
+    per_iter = bytes_b + bytes_h + 88 * N
+    return iters * per_iter + applies * (bytes_b + bytes_h + 24 * N), per_iter
 
 
 class ClockSampler:
@@ -123,7 +172,7 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_baseline(op, rhs, iters: int):
+def cpu_baseline(op, rhs, iters: int, name: str = "cfg5"):
     """The reference path (oracle restatement, bit-identical to qpipm on the
     golden vectors) on a bounded sample: `iters` PCG iterations of cfg5."""
     from oracle import qp_oracle as orc
@@ -133,7 +182,7 @@ def cpu_baseline(op, rhs, iters: int):
     dt = time.perf_counter() - t0
     # iterations + the final true-residual apply, as in the GPU step
     return {"value": iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{iters} PCG iterations of cfg5 (+ Jacobi build + final apply), {dt:.1f} s; "
+            "sample": f"{iters} PCG iterations of {name} (+ Jacobi build + final apply), {dt:.1f} s; "
                       f"numpy/scipy oracle bit-identical to qpipm; sparse matvecs single-threaded "
                       f"({len(os.sched_getaffinity(0))} host cores visible)"}
 
@@ -142,9 +191,8 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    problem, op, meta = make_workload(args.scale)
+    problem, op, rhs, meta = make_workload(args.workload, args.scale)
     from oracle import qp_oracle as orc
-    rhs = meta["rhs"]
     k_iter = args.ref_iters_per_step
     orc.jacobi_diagonal(op)
     for _ in range(args.warmup):
@@ -158,10 +206,10 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg5 operator sweep 4Mx1M, 16 nnz/row, log10 w ~ U(-6,6)",
-                   "pcg_iters_per_step": k_iter, "seed": meta["seed"]},
+        "config": {"workload": WORKLOAD_DESC[args.workload], "pcg_iters_per_step": k_iter,
+                   "seed": meta["seed"]},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{k_iter} PCG iterations per step of cfg5 through the oracle "
+                         "sample": f"{k_iter} PCG iterations per step of {args.workload} through the oracle "
                                    f"(numpy/scipy restatement of qpipm, bit-identical on golden vectors)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -179,8 +227,7 @@ def run_ours(args):
     from paper_2308_00637_b200.direction import GpuKkt, gpu_direction, operator_for
     from paper_2308_00637_b200.pcg import PcgConfig
 
-    problem, op, meta = make_workload(args.scale, seed=5 + rank)
-    rhs = meta["rhs"]
+    problem, op, rhs, meta = make_workload(args.workload, args.scale, seed_offset=rank)
     gk = GpuKkt(problem, op.bmap, device=local, scatter=args.scatter)
     stream = torch.cuda.current_stream()
     gk.ctx.call("qpk_set_stream", _native.ctypes.c_void_p(stream.cuda_stream))
@@ -188,10 +235,15 @@ def run_ours(args):
     gk.jacobi()
     N = op.dim
     rhs_d = torch.from_numpy(rhs).to(f"cuda:{local}")
+    d_d = torch.from_numpy(np.ascontiguousarray(op.d_diag)).to(f"cuda:{local}")
+    q_d = torch.from_numpy(np.ascontiguousarray(op.q_diag_extra)).to(f"cuda:{local}")
     x_d = torch.empty(N, dtype=torch.float64, device=f"cuda:{local}")
     info = _native.PcgInfo()
 
     def step():
+        # one IPM iteration's device work: new diagonals (marks the Jacobi
+        # diagonal stale -> rebuilt), then the fixed-iteration PCG solve
+        gk.ctx.call("qpk_set_diagonals_dev", d_d.data_ptr(), q_d.data_ptr())
         gk.ctx.call("qpk_pcg_dev", rhs_d.data_ptr(), 1e-300, 1, args.iters, x_d.data_ptr(),
                     _native.ctypes.byref(info), None)
 
@@ -264,11 +316,13 @@ def run_ours(args):
             "warmup": max(args.warmup, 3), "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator of BASELINE.json configs[4]; no dataset involved)",
-            "config": {"workload": f"cfg5 operator sweep {op.m}x{op.n}, 16 nnz/row, H=diag(U(1e-2,1)), "
-                                   f"log10 w ~ U(-6,6); {args.iters} PCG iterations per step",
+            "config": {"workload": WORKLOAD_DESC[args.workload] + (f" (scale {args.scale})" if args.scale != 1 else "")
+                                   + f"; {args.iters} PCG iterations per step (+ Jacobi build + final apply)",
                        "parallelism": "replicas" if world > 1 else "single",
                        "scatter": "atomic" if args.scatter == 1 else "csc",
-                       "l2": "inputs larger than L2 (B alone 0.78 GB vs 126 MB L2)",
+                       "l2": "inputs larger than L2" if per_iter > 126e6 else
+                       "working set fits L2 (each step re-reads it every PCG iteration; no flush)",
+                       "n": op.n, "m_B": op.m, "nnz_B": gk.ctx.query("nnz"),
                        "grid": gk.ctx.query("grid"), "lanes_per_row": gk.ctx.query("lanes"),
                        "seed": meta["seed"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -284,7 +338,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(op, rhs, args.cpu_iters)
+            line["cpu_baseline"] = cpu_baseline(op, rhs, args.cpu_iters, args.workload)
         print(json.dumps(line), flush=True)
     gk.close()
     if world > 1:
