@@ -61,8 +61,11 @@ enum { QPK_PCG_OK = 0, QPK_PCG_BREAKDOWN = 1 };
 enum {
   QPK_SCATTER_AUTO = 0,    /* chosen per matrix at finalize */
   QPK_SCATTER_ATOMIC = 1,  /* one pass over B, fp64 atomics (order not reproducible) */
-  QPK_SCATTER_CSC = 2      /* second, gather-only pass over a resident CSC copy:
+  QPK_SCATTER_CSC = 2,     /* second, gather-only pass over a resident CSC copy:
                               bitwise reproducible run to run */
+  QPK_SCATTER_DICT = 3     /* one pass; rows grouped into blocks with a shared-memory
+                              column dictionary, per-block partials combined in a
+                              fixed order: no atomics, bitwise reproducible */
 };
 
 typedef struct qpk_ctx qpk_ctx;

@@ -24,6 +24,7 @@
 
 #include "../../include/qpk.h"
 #include "qpk_device.cuh"
+#include "qpk_engine.cuh"
 
 namespace cg = cooperative_groups;
 using namespace qpk;
@@ -35,17 +36,12 @@ struct PcgOut {
   unsigned long long phase_ns[4];
 };
 
-__device__ __forceinline__ unsigned long long globaltimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 
 // per-phase wall time as seen by block 0 (includes waiting for the slowest block)
 struct PhaseClock {
   unsigned long long last = 0, acc[4] = {0, 0, 0, 0};
-  __device__ void start() { last = globaltimer(); }
-  __device__ void lap(int phase) { const unsigned long long t = globaltimer(); acc[phase] += t - last; last = t; }
+  __device__ void start() { last = globaltimer_ns(); }
+  __device__ void lap(int phase) { const unsigned long long t = globaltimer_ns(); acc[phase] += t - last; last = t; }
 };
 
 struct PcgParams {
@@ -447,7 +443,16 @@ struct qpk_ctx {
   int lanes = 4, csc_lanes = 8, h_lanes = 8;
 
   // device problem
-  DBuf<int> rp, ci, cp, ri, hrp, hci;
+  DBuf<int> rp, ci, cp, ri, hrp, hci, seg_ptr, seg_beg;
+  DBuf<double> seg_sum;
+  int n_seg = 0, seg_lanes = 8;
+  // row-block dictionaries
+  DBuf<int> blk_row, blk_dict, dcols, col_ptr, col_pos;
+  DBuf<unsigned short> lci;
+  DBuf<double> bpart;
+  int nblk = 0;
+  bool have_dict = false;
+  double dict_reuse = 0.0;
   DBuf<double> bv, cv, hh, hv, hdense, U, w, hdiag;
   bool have_csc = false;
 
@@ -459,6 +464,18 @@ struct qpk_ctx {
   DBuf<double> x[3], r, p, y, zb, rhs, part, hist, vin;
   DBuf<PcgOut> out;
   int grid_pcg = 0, grid_std = 0;
+
+  // slot engine
+  int engine = -1;               // -1 auto, 0 persistent kernel, 1 slot engine
+  int grid_eng = 0;
+  DBuf<Ctrl> ctrl;
+  DBuf<unsigned int> counter;
+  DBuf<EngineCfg> ecfg;
+  int* pinned_mode = nullptr;    // [2] host-mapped poll flags
+  cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  cudaGraphExec_t graph = nullptr;
+  int graph_slots = 0;
+  bool graph_failed = false;
 
   Op op() const {
     Op o;
@@ -479,6 +496,10 @@ static cudaError_t upload(DBuf<T>& dst, const std::vector<T>& src, cudaStream_t 
   if (e != cudaSuccess || src.empty()) return e;
   return cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
+
+static constexpr int DICT_SMEM = (1 + QPK_DICT_WARPS) * QPK_DICT_MAX * (int)sizeof(double);
+static int engine_setup(qpk_ctx* c);
+static Engine make_engine(qpk_ctx* c);
 
 // ---------------------------------------------------------- dispatchers ---
 template <int L, bool CSC>
@@ -550,6 +571,9 @@ int qpk_destroy(qpk_ctx* c) {
   if (!c) return QPK_OK;
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto& e : c->poll_ev) if (e) cudaEventDestroy(e);
+  if (c->pinned_mode) cudaFreeHost(c->pinned_mode);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
   return QPK_OK;
@@ -676,13 +700,104 @@ static int build_csc(qpk_ctx* c) {
       ri[at] = (int)r;
       cv[at] = c->h_v[k];
     }
+  // column segments for the engine's B'z pass: LS lanes x 8 entries each
+  {
+    const long long avg = tot / std::max<long long>(n, 1);
+    c->seg_lanes = pow2_clamp((avg + 7) / 8, 1, 32);
+    if (const char* ev = getenv("QPK_SEG_LANES")) c->seg_lanes = pow2_clamp(atoi(ev), 1, 32);
+    const int seg = 8 * c->seg_lanes;
+    std::vector<int> sp(n + 1), sb;
+    sb.reserve(tot / seg + n + 1);
+    for (long long j = 0; j < n; ++j) {
+      sp[j] = (int)sb.size();
+      for (int b = cp[j]; b < cp[j + 1]; b += seg) sb.push_back(b);
+    }
+    sp[n] = (int)sb.size();
+    sb.push_back(cp[n]);
+    c->n_seg = sp[n];
+    // each segment ends where the next one (or the next column) begins
+    CUDA_TRY(upload(c->seg_ptr, sp, c->stream));
+    CUDA_TRY(upload(c->seg_beg, sb, c->stream));
+    CUDA_TRY(c->seg_sum.alloc(std::max(c->n_seg, 1)));
+  }
   CUDA_TRY(upload(c->cp, cp, c->stream));
   CUDA_TRY(upload(c->ri, ri, c->stream));
   CUDA_TRY(upload(c->cv, cv, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   // lanes per column: ~16 entries (4 chunks) per lane
   c->csc_lanes = pow2_clamp((tot / std::max<long long>(n, 1) + 15) / 16, 1, 32);
+  if (const char* ev = getenv("QPK_CSC_LANES")) c->csc_lanes = pow2_clamp(atoi(ev), 1, 32);
   c->have_csc = true;
+  return QPK_OK;
+}
+
+// Row blocks of <= QPK_DICT_ROWS rows whose distinct columns fit a
+// QPK_DICT_MAX-entry shared-memory dictionary; entries re-indexed to 16 bits.
+// Returns QPK_OK with have_dict = false when a row alone exceeds the limit.
+static int build_dict(qpk_ctx* c) {
+  c->have_dict = false;
+  const long long n = c->n, m = c->m;
+  std::vector<int> mark(n, -1), local(n, 0);
+  std::vector<int> blk_row(1, 0), blk_dict(1, 0), cols, cur;
+  std::vector<unsigned short> lci(c->h_ci.size(), 0xFFFF);
+  cur.reserve(QPK_DICT_MAX);
+  int blk = 0;
+  long long rows_in = 0;
+  auto close_block = [&](long long r_end) {
+    std::vector<int> order(cur.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return cur[a] < cur[b]; });
+    std::vector<int> newpos(cur.size());
+    for (size_t i = 0; i < order.size(); ++i) newpos[order[i]] = (int)i;
+    for (long long r = blk_row.back(); r < r_end; ++r)
+      for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k)
+        if (c->h_ci[k] >= 0) lci[k] = (unsigned short)newpos[lci[k]];
+    for (int i : order) cols.push_back(cur[i]);
+    blk_dict.push_back((int)cols.size());
+    blk_row.push_back((int)r_end);
+    ++blk;
+    cur.clear();
+    rows_in = 0;
+  };
+  for (long long r = 0; r < m; ++r) {
+    int fresh = 0, len = 0;
+    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+      const int col = c->h_ci[k];
+      if (col < 0) continue;
+      ++len;
+      if (mark[col] != blk) ++fresh;
+    }
+    if (len > QPK_DICT_MAX) return QPK_OK;                 // row too wide for a dictionary
+    if (rows_in > 0 && (rows_in >= QPK_DICT_ROWS || (long long)cur.size() + fresh > QPK_DICT_MAX)) close_block(r);
+    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+      const int col = c->h_ci[k];
+      if (col < 0) continue;
+      if (mark[col] != blk) { mark[col] = blk; local[col] = (int)cur.size(); cur.push_back(col); }
+      lci[k] = (unsigned short)local[col];
+    }
+    ++rows_in;
+  }
+  if (rows_in > 0) close_block(m);
+  // column -> its dictionary positions, in block order
+  std::vector<int> col_ptr(n + 1, 0), col_pos(cols.size());
+  for (int col : cols) col_ptr[col + 1]++;
+  for (long long j = 0; j < n; ++j) col_ptr[j + 1] += col_ptr[j];
+  {
+    std::vector<int> at(col_ptr.begin(), col_ptr.end() - 1);
+    for (size_t p = 0; p < cols.size(); ++p) col_pos[at[cols[p]]++] = (int)p;
+  }
+  cudaStream_t s = c->stream;
+  CUDA_TRY(upload(c->blk_row, blk_row, s));
+  CUDA_TRY(upload(c->blk_dict, blk_dict, s));
+  CUDA_TRY(upload(c->dcols, cols, s));
+  CUDA_TRY(upload(c->lci, lci, s));
+  CUDA_TRY(upload(c->col_ptr, col_ptr, s));
+  CUDA_TRY(upload(c->col_pos, col_pos, s));
+  CUDA_TRY(c->bpart.alloc(std::max<size_t>(cols.size(), 1)));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  c->nblk = blk;
+  c->dict_reuse = cols.empty() ? 0.0 : (double)c->nnz / (double)cols.size();
+  c->have_dict = true;
   return QPK_OK;
 }
 
@@ -721,12 +836,25 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   CUDA_TRY(c->vin.alloc(N));
   CUDA_TRY(c->zb.alloc(std::max<long long>(c->m, 1)));
 
-  c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 4, 1, 32);
-  // B'z strategy: atomic scatter by default; CSC when asked (deterministic)
-  c->scatter = (scatter == QPK_SCATTER_CSC) ? QPK_SCATTER_CSC : QPK_SCATTER_ATOMIC;
-  if (c->scatter == QPK_SCATTER_CSC) {
+  // lanes per row: ~3 chunks of 4 nonzeros per lane keeps several gathers in flight
+  c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 12, 1, 32);
+  if (const char* ev = getenv("QPK_LANES")) c->lanes = pow2_clamp(atoi(ev), 1, 32);
+  // B'z strategy.  AUTO: the row-block dictionary when blocks reuse their
+  // columns (banded / clustered B: RT, SVM, dense), else one-pass atomics
+  // (random B, where no blocking creates reuse).  CSC and DICT are
+  // deterministic; DICT falls back to CSC when a row is wider than a dictionary.
+  if (const char* ev = getenv("QPK_SCATTER")) if (scatter == QPK_SCATTER_AUTO) scatter = atoi(ev);
+  c->scatter = QPK_SCATTER_ATOMIC;
+  if ((scatter == QPK_SCATTER_AUTO || scatter == QPK_SCATTER_DICT) && c->m > 0) {
+    int rc = build_dict(c);
+    if (rc) return rc;
+    if (c->have_dict && scatter == QPK_SCATTER_DICT) c->scatter = QPK_SCATTER_DICT;
+    else if (scatter == QPK_SCATTER_DICT || (c->have_dict && c->dict_reuse >= 4.0)) scatter = QPK_SCATTER_CSC;
+  }
+  if (scatter == QPK_SCATTER_CSC && c->m > 0) {
     int rc = build_csc(c);
     if (rc) return rc;
+    c->scatter = QPK_SCATTER_CSC;
   }
 
   // grid sizes: persistent kernel = all co-resident blocks (capped by work)
@@ -737,7 +865,13 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   const long long work = std::max<long long>((long long)c->h_ci.size() / 1024, N / 512);
   c->grid_pcg = (int)std::max<long long>(1, std::min<long long>((long long)per_sm * c->sms, work));
   c->grid_std = c->grid_pcg;
-  CUDA_TRY(c->part.alloc((size_t)NSLOTS * c->grid_pcg));
+  {
+    int eng_per_sm = c->scatter == QPK_SCATTER_DICT ? 3 : 4;
+    const long long ework = std::max<long long>((long long)c->h_ci.size() / 512, N / 256);
+    c->grid_eng = (int)std::max<long long>(1, std::min<long long>((long long)eng_per_sm * c->sms, ework));
+  }
+  CUDA_TRY(c->part.alloc((size_t)NSLOTS * std::max(c->grid_pcg, c->grid_eng)));
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
 
   Op o = c->op();
   k_hdiag<<<std::max(1, std::min(c->sms * 4, (int)((c->n + 255) / 256))), 256, 0, s>>>(o.H, (int)c->n, c->hdiag.p);
@@ -779,6 +913,17 @@ static int build_jacobi(qpk_ctx* c) {
   Op o = c->op();
   const int G = c->grid_std;
   cudaStream_t s = c->stream;
+  if (c->scatter == QPK_SCATTER_DICT) {
+    int rc = engine_setup(c);
+    if (rc) return rc;
+    Engine E = make_engine(c);
+    k_jac_dict<<<c->grid_eng, QPK_DICT_WARPS * 32, DICT_SMEM, s>>>(E);
+    k_jac_dict_finish<<<G, QPK_BLOCK, 0, s>>>(E, c->hdiag.p, c->jac.p, c->minv.p);
+    c->launches += 2;
+    CUDA_TRY(cudaGetLastError());
+    c->jac_ready = true;
+    return QPK_OK;
+  }
   CUDA_TRY(cudaMemsetAsync(c->y.p, 0, c->n * sizeof(double), s));
   if (c->m) {
     if (c->have_csc) k_jac_cols<<<G, QPK_BLOCK, 0, s>>>(o, c->y.p);
@@ -838,31 +983,186 @@ int qpk_apply_dev(qpk_ctx* c, const double* v, double* y) {
   return apply_impl(c, v, y);
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------ slot engine ---
+template <int L, bool CSC>
+static void launch_slot_rows_t(int grid, cudaStream_t s, const Engine& E, int par) {
+  k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
+}
+
+static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
+  const bool csc = c->scatter == QPK_SCATTER_CSC;
+  const int G = c->grid_eng;
+  k_slot_top<<<G, QPK_BLOCK, 0, s>>>(E, par);
+  if (c->scatter == QPK_SCATTER_DICT) {
+    k_slot_rows_dict<<<G, QPK_DICT_WARPS * 32, DICT_SMEM, s>>>(E, par);
+    k_slot_update<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
+    return;
+  }
+  switch (c->lanes * 2 + (csc ? 1 : 0)) {
+    case 2: launch_slot_rows_t<1, false>(G, s, E, par); break;
+    case 3: launch_slot_rows_t<1, true>(G, s, E, par); break;
+    case 4: launch_slot_rows_t<2, false>(G, s, E, par); break;
+    case 5: launch_slot_rows_t<2, true>(G, s, E, par); break;
+    case 8: launch_slot_rows_t<4, false>(G, s, E, par); break;
+    case 9: launch_slot_rows_t<4, true>(G, s, E, par); break;
+    case 16: launch_slot_rows_t<8, false>(G, s, E, par); break;
+    case 17: launch_slot_rows_t<8, true>(G, s, E, par); break;
+    case 32: launch_slot_rows_t<16, false>(G, s, E, par); break;
+    case 33: launch_slot_rows_t<16, true>(G, s, E, par); break;
+    case 64: launch_slot_rows_t<32, false>(G, s, E, par); break;
+    default: launch_slot_rows_t<32, true>(G, s, E, par); break;
+  }
+  if (csc) {
+    k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
+    k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  }
+  else k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+}
+
+static Engine make_engine(qpk_ctx* c) {
+  Engine E;
+  E.op = c->op();
+  E.rhs = c->rhs.p;
+  for (int i = 0; i < 3; ++i) E.x[i] = c->x[i].p;
+  E.r = c->r.p; E.p = c->p.p; E.y = c->y.p; E.zb = c->zb.p; E.minv = c->minv.p;
+  E.part = c->part.p; E.G = c->grid_eng;
+  E.ctrl = c->ctrl.p; E.counter = c->counter.p; E.cfg = c->ecfg.p;
+  E.seg_ptr = c->seg_ptr.p; E.seg_beg = c->seg_beg.p; E.seg_sum = c->seg_sum.p;
+  E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
+  E.scatter = c->scatter;
+  E.dict.nblk = c->nblk; E.dict.blk_row = c->blk_row.p; E.dict.blk_dict = c->blk_dict.p; E.dict.cols = c->dcols.p;
+  E.dict.lci = c->lci.p; E.dict.bpart = c->bpart.p; E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
+  return E;
+}
+
+static int engine_setup(qpk_ctx* c) {
+  if (c->ctrl.p) return QPK_OK;
+  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(k_jac_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
+  CUDA_TRY(c->ctrl.alloc(2));
+  CUDA_TRY(c->counter.alloc(1));
+  CUDA_TRY(c->ecfg.alloc(1));
+  CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned int), c->stream));
+  CUDA_TRY(cudaMemsetAsync(c->ctrl.p, 0, 2 * sizeof(Ctrl), c->stream));
+  CUDA_TRY(cudaHostAlloc((void**)&c->pinned_mode, 2 * sizeof(int), cudaHostAllocDefault));
+  for (auto& e : c->poll_ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return QPK_OK;
+}
+
+// capture `slots` identical slots (slots even: parity pattern repeats) as a graph
+static int engine_graph(qpk_ctx* c, int slots) {
+  if (c->graph && c->graph_slots == slots) return QPK_OK;
+  if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+  if (c->graph_failed) return QPK_OK;
+  Engine E = make_engine(c);
+  cudaStream_t cs = c->own;
+  cudaGraph_t g = nullptr;
+  if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { c->graph_failed = true; cudaGetLastError(); return QPK_OK; }
+  for (int s = 0; s < slots; ++s) launch_slot(c, E, s & 1, cs);
+  if (cudaStreamEndCapture(cs, &g) != cudaSuccess || !g) { c->graph_failed = true; cudaGetLastError(); return QPK_OK; }
+  if (cudaGraphInstantiate(&c->graph, g, 0) != cudaSuccess) { c->graph = nullptr; c->graph_failed = true; cudaGetLastError(); }
+  cudaGraphDestroy(g);
+  c->graph_slots = slots;
+  return QPK_OK;
+}
+
+static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double* hist_dev, PcgOut* out) {
+  int rc = engine_setup(c);
+  if (rc) return rc;
+  const int CH = 16;
+  rc = engine_graph(c, CH);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  EngineCfg hc;
+  hc.tol = tol; hc.max_iters = max_iters; hc.rel = rel ? 1 : 0; hc.pad = 0; hc.hist = hist_dev;
+  CUDA_TRY(cudaMemcpyAsync(c->ecfg.p, &hc, sizeof hc, cudaMemcpyHostToDevice, s));
+  Engine E = make_engine(c);
+  k_engine_init<<<c->grid_eng, QPK_BLOCK, 0, s>>>(E);
+  c->launches++;
+  CUDA_TRY(cudaGetLastError());
+  // upper bound on slots: every iteration may be followed by a check, + final
+  const long long max_slots = 2 * max_iters + 4;
+  long long slots = 0;
+  int chunk = 0;
+  for (;;) {
+    if (c->graph) {
+      CUDA_TRY(cudaGraphLaunch(c->graph, s));
+    } else {
+      for (int k = 0; k < CH; ++k) launch_slot(c, E, k & 1, s);
+    }
+    c->launches += (c->scatter == QPK_SCATTER_CSC ? 4 : 3) * CH;
+    slots += CH;
+    const int b = chunk & 1;
+    CUDA_TRY(cudaMemcpyAsync(&c->pinned_mode[b], &c->ctrl.p[0].mode, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaEventRecord(c->poll_ev[b], s));
+    if (chunk > 0) {
+      CUDA_TRY(cudaEventSynchronize(c->poll_ev[b ^ 1]));
+      if (c->pinned_mode[b ^ 1] == MODE_DONE) break;
+    }
+    if (slots > max_slots + 2 * CH) return fail(QPK_E_STATE, "slot engine did not terminate");
+    ++chunk;
+  }
+  Ctrl fin;
+  CUDA_TRY(cudaMemcpyAsync(&fin, c->ctrl.p, sizeof fin, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  CUDA_TRY(cudaGetLastError());
+  if (fin.mode != MODE_DONE) return fail(QPK_E_STATE, "slot engine: final state not DONE");
+  out->iterations = fin.k; out->converged = fin.converged; out->status = fin.status;
+  out->restarts = fin.restarts; out->applies = fin.applies; out->result_buf = fin.result;
+  out->final_norm = fin.final_norm; out->threshold = fin.thr; out->rhs_norm = fin.rhs_norm;
+  out->phase_ns[0] = fin.ph[0]; out->phase_ns[1] = fin.ph[1]; out->phase_ns[2] = fin.ph[2]; out->phase_ns[3] = 0;
+  return QPK_OK;
+}
+
+extern "C" {
+
+static bool use_engine(qpk_ctx* c) {
+  if (c->scatter == QPK_SCATTER_DICT) return true;   // only the slot engine has the dictionary kernels
+  if (c->engine >= 0) return c->engine == 1;
+  const char* env = getenv("QPK_ENGINE");
+  if (env) return atoi(env) == 1;
+  // small systems: one cooperative launch wins on latency; the random-B atomic
+  // path is as fast in the persistent kernel; the CSC path needs the engine's
+  // balanced column segments
+  return c->scatter == QPK_SCATTER_CSC && c->N() >= 50000;
+}
+
 static int pcg_impl(qpk_ctx* c, const double* rhs_dev, double tol, int rel, int64_t max_iters, double* x_dev,
                     qpk_pcg_info* info, double* hist_dev) {
   if (!(tol > 0.0)) return fail(QPK_E_ARG, "tol must be positive");
   if (max_iters < 1) return fail(QPK_E_ARG, "max_iters must be at least 1");
+  if (max_iters > (1LL << 30)) return fail(QPK_E_ARG, "max_iters too large");
   if (!c->jac_ready) { int rc = build_jacobi(c); if (rc) return rc; }
-  PcgParams P;
-  P.op = c->op();
-  P.rhs = rhs_dev;
-  P.x0 = c->x[0].p; P.x1 = c->x[1].p; P.x2 = c->x[2].p;
-  P.r = c->r.p; P.p = c->p.p; P.y = c->y.p; P.zb = c->zb.p; P.minv = c->minv.p;
-  P.part = c->part.p; P.G = c->grid_pcg;
-  P.tol = tol; P.rel = rel ? 1 : 0; P.max_iters = max_iters;
-  P.hist = hist_dev;
-  P.out = c->out.p;
-  void* args[] = {&P};
+  if (rhs_dev != c->rhs.p)
+    CUDA_TRY(cudaMemcpyAsync(c->rhs.p, rhs_dev, c->N() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   cudaEvent_t e0, e1;
   CUDA_TRY(cudaEventCreate(&e0));
   CUDA_TRY(cudaEventCreate(&e1));
   CUDA_TRY(cudaEventRecord(e0, c->stream));
-  CUDA_TRY(cudaLaunchCooperativeKernel(pcg_kernel_for(c->lanes, c->scatter == QPK_SCATTER_CSC),
-                                       dim3(c->grid_pcg), dim3(QPK_BLOCK), args, 0, c->stream));
-  c->launches++;
-  CUDA_TRY(cudaEventRecord(e1, c->stream));
   PcgOut o;
-  CUDA_TRY(cudaMemcpyAsync(&o, c->out.p, sizeof o, cudaMemcpyDeviceToHost, c->stream));
+  if (use_engine(c)) {
+    int rc = pcg_engine(c, tol, rel, max_iters, hist_dev, &o);
+    if (rc) return rc;
+    CUDA_TRY(cudaEventRecord(e1, c->stream));
+  } else {
+    PcgParams P;
+    P.op = c->op();
+    P.rhs = c->rhs.p;
+    P.x0 = c->x[0].p; P.x1 = c->x[1].p; P.x2 = c->x[2].p;
+    P.r = c->r.p; P.p = c->p.p; P.y = c->y.p; P.zb = c->zb.p; P.minv = c->minv.p;
+    P.part = c->part.p; P.G = c->grid_pcg;
+    P.tol = tol; P.rel = rel ? 1 : 0; P.max_iters = max_iters;
+    P.hist = hist_dev;
+    P.out = c->out.p;
+    void* args[] = {&P};
+    CUDA_TRY(cudaLaunchCooperativeKernel(pcg_kernel_for(c->lanes, c->scatter == QPK_SCATTER_CSC),
+                                         dim3(c->grid_pcg), dim3(QPK_BLOCK), args, 0, c->stream));
+    c->launches++;
+    CUDA_TRY(cudaEventRecord(e1, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&o, c->out.p, sizeof o, cudaMemcpyDeviceToHost, c->stream));
+  }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
@@ -927,6 +1227,10 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "csc_lanes") return c->csc_lanes;
   if (k == "scatter") return c->scatter;
   if (k == "grid") return c->grid_pcg;
+  if (k == "grid_engine") return c->grid_eng;
+  if (k == "engine") return use_engine(c) ? 1 : 0;
+  if (k == "dict_blocks") return c->nblk;
+  if (k == "dict_reuse_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "block") return QPK_BLOCK;
   if (k == "sms") return c->sms;
   if (k == "hess_kind") return c->hkind;

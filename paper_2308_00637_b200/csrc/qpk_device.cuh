@@ -46,6 +46,12 @@ struct Op {
 enum { SLOT_ROWS = 0, SLOT_PREP = 1, SLOT_RR = 2, SLOT_RZ = 3, SLOT_AUX = 4, SLOT_AUX2 = 5, SLOT_S = 6,
        NSLOTS = SLOT_S + QPK_KMAX };
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // ---------------------------------------------------------------- loads ----
 __device__ __forceinline__ int4 ld_stream_i4(const int* p) {
   int4 r;
@@ -154,84 +160,14 @@ struct RowFuse {
 // part H u (CSR / dense / low-rank) is added to y_top.  Accumulates
 // t z + w y_bottom (+ u'H u) so that v'Kv is known after this phase:
 //   v'Kv = u'Q u + sum_r z_r t_r + sum_r w_r y_r   (since u'B'z = t'z).
-template <int L, bool CSC, bool FUSE>
-__device__ void phase_rows(const Op& op, double* v, double* y, double* zb,
-                           double* part, int G, double* red, double* s_lr, const RowFuse& f) {
-  const double* u = v;
-  double* w = v + op.n;
-  double acc = 0.0, rzb = 0.0;
-  const int lane = threadIdx.x & (L - 1);
-  constexpr int RPW = 32 / L;                       // rows per warp step
+// Non-diagonal Hessian part of Q u (CSR / dense / low-rank), atomically added
+// to y_top; returns this thread's share of u'H'u (H' = H minus its diagonal
+// part handled in prep).  Grid-stride over the rows of H.
+__device__ __forceinline__ double hess_rows(const Op& op, const double* u, double* y, const double* part, int G,
+                                            double* red, double* s_lr) {
+  double acc = 0.0;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarp = (gridDim.x * blockDim.x) >> 5;
-  const int sub_in_warp = (threadIdx.x & 31) / L;
-  for (long long rb = (long long)gwarp * RPW; rb < op.m; rb += (long long)nwarp * RPW) {
-    const int r = (int)rb + sub_in_warp;
-    const bool active = r < op.m;
-    int b = 0, e = 0;
-    double dr = 1.0, wr = 0.0;
-    if (active) {
-      b = __ldg(op.rp + r); e = __ldg(op.rp + r + 1);
-      dr = __ldg(op.d + r);
-      wr = w[r];
-      if (FUSE) {
-        // every lane of the row computes the same values; lane 0 stores
-        const double rr = f.r[op.n + r];
-        const double zr = __dmul_rn(1.0 / dr, rr);
-        if (f.xupd && lane == 0) f.xdst[op.n + r] = __dadd_rn(f.xsrc[op.n + r], __dmul_rn(f.alpha_prev, wr));
-        const double pn = f.restart ? zr : __dadd_rn(zr, __dmul_rn(f.beta, wr));
-        if (lane == 0) { w[r] = pn; rzb += rr * zr; }
-        wr = pn;
-      }
-    }
-    const int k0 = b + 4 * lane;
-    int4 c0 = make_int4(-1, -1, -1, -1);
-    double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
-    if (k0 < e) { c0 = ld_stream_i4(op.ci + k0); v0 = ld_stream_d2(op.bv + k0); v1 = ld_stream_d2(op.bv + k0 + 2); }
-    double s = 0.0;
-    if (c0.x >= 0) s = fma(v0.x, u[c0.x], s);
-    if (c0.y >= 0) s = fma(v0.y, u[c0.y], s);
-    if (c0.z >= 0) s = fma(v1.x, u[c0.z], s);
-    if (c0.w >= 0) s = fma(v1.y, u[c0.w], s);
-    for (int k = k0 + 4 * L; k < e; k += 4 * L) {   // rows longer than 4L nonzeros
-      int4 c = ld_stream_i4(op.ci + k);
-      double2 a0 = ld_stream_d2(op.bv + k), a1 = ld_stream_d2(op.bv + k + 2);
-      if (c.x >= 0) s = fma(a0.x, u[c.x], s);
-      if (c.y >= 0) s = fma(a0.y, u[c.y], s);
-      if (c.z >= 0) s = fma(a1.x, u[c.z], s);
-      if (c.w >= 0) s = fma(a1.y, u[c.w], s);
-    }
-    const double t = subwarp_sum<L>(s);
-    if (!active) continue;
-    const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
-    const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
-    if (lane == 0) {
-      y[op.n + r] = yb;
-      acc += t * z + wr * yb;
-      if (CSC) zb[r] = z;
-    }
-    if (!CSC) {
-      if (c0.x >= 0) atomicAdd(y + c0.x, z * v0.x);
-      if (c0.y >= 0) atomicAdd(y + c0.y, z * v0.y);
-      if (c0.z >= 0) atomicAdd(y + c0.z, z * v1.x);
-      if (c0.w >= 0) atomicAdd(y + c0.w, z * v1.y);
-      for (int k = k0 + 4 * L; k < e; k += 4 * L) {
-        int4 c = *reinterpret_cast<const int4*>(op.ci + k);
-        double2 a0 = *reinterpret_cast<const double2*>(op.bv + k);
-        double2 a1 = *reinterpret_cast<const double2*>(op.bv + k + 2);
-        if (c.x >= 0) atomicAdd(y + c.x, z * a0.x);
-        if (c.y >= 0) atomicAdd(y + c.y, z * a0.y);
-        if (c.z >= 0) atomicAdd(y + c.z, z * a1.x);
-        if (c.w >= 0) atomicAdd(y + c.w, z * a1.y);
-      }
-    }
-  }
-  if (FUSE) {
-    const double t2 = block_sum(rzb, red);
-    if (threadIdx.x == 0) part[SLOT_AUX2 * G + blockIdx.x] = t2;
-  }
-
-  // non-diagonal Hessian part, added to y_top
   const int kind = op.H.kind;
   if (kind == HESS_CSR) {
     const int LH = op.H.lanes;                       // power of two <= 32
@@ -276,6 +212,195 @@ __device__ void phase_rows(const Op& op, double* v, double* y, double* zb,
       atomicAdd(y + j, s);
     }
   }
+  return acc;
+}
+
+template <int L>
+__device__ __forceinline__ void load_chunk(const Op& op, int k, int e, int4& c, double2& v0, double2& v1) {
+  c = make_int4(-1, -1, -1, -1);
+  v0 = make_double2(0.0, 0.0);
+  v1 = v0;
+  if (k < e) { c = ld_stream_i4(op.ci + k); v0 = ld_stream_d2(op.bv + k); v1 = ld_stream_d2(op.bv + k + 2); }
+}
+
+// B-row loop, software-pipelined: while step i's gathers are in flight the
+// index/value chunk of step i+1 and the row pointers of step i+2 load.
+// Returns this thread's partial of t z + w y_b; *rzb gets r_b z_b (FUSE).
+template <int L, bool CSC, bool FUSE>
+__device__ __forceinline__ double rows_loop_pipelined(const Op& op, double* v, double* y, double* zb,
+                                                      const RowFuse& f, double* rzb_out) {
+  const double* u = v;
+  double* w = v + op.n;
+  double acc = 0.0, rzb = 0.0;
+  const int lane = threadIdx.x & (L - 1);
+  constexpr int RPW = 32 / L;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  const int sub = (threadIdx.x & 31) / L;
+  const long long step = (long long)nwarp * RPW;
+  long long rb = (long long)gwarp * RPW;
+  int r = (int)rb + sub;
+  bool act = rb < op.m && r < op.m;
+  int b = 0, e = 0;
+  if (act) { b = __ldg(op.rp + r); e = __ldg(op.rp + r + 1); }
+  int4 c0; double2 v0, v1;
+  load_chunk<L>(op, b + 4 * lane, e, c0, v0, v1);
+  long long rb1 = rb + step;
+  int r1 = (int)rb1 + sub;
+  bool act1 = rb1 < op.m && r1 < op.m;
+  int b1 = 0, e1 = 0;
+  if (act1) { b1 = __ldg(op.rp + r1); e1 = __ldg(op.rp + r1 + 1); }
+  for (; rb < op.m; rb += step) {
+    int4 cn; double2 vn0, vn1;
+    load_chunk<L>(op, b1 + 4 * lane, e1, cn, vn0, vn1);
+    const long long rb2 = rb1 + step;
+    const int r2 = (int)rb2 + sub;
+    const bool act2 = rb2 < op.m && r2 < op.m;
+    int b2 = 0, e2 = 0;
+    if (act2) { b2 = __ldg(op.rp + r2); e2 = __ldg(op.rp + r2 + 1); }
+    double dr = 1.0, wr = 0.0, rres = 0.0, xs = 0.0;
+    if (act) {
+      dr = __ldg(op.d + r);
+      wr = w[r];
+      if (FUSE) {
+        rres = f.r[op.n + r];
+        if (f.xupd && lane == 0) xs = f.xsrc[op.n + r];
+      }
+    }
+    double s = 0.0;
+    if (c0.x >= 0) s = fma(v0.x, u[c0.x], s);
+    if (c0.y >= 0) s = fma(v0.y, u[c0.y], s);
+    if (c0.z >= 0) s = fma(v1.x, u[c0.z], s);
+    if (c0.w >= 0) s = fma(v1.y, u[c0.w], s);
+    for (int k = b + 4 * lane + 4 * L; k < e; k += 4 * L) {
+      int4 c = ld_stream_i4(op.ci + k);
+      double2 a0 = ld_stream_d2(op.bv + k), a1 = ld_stream_d2(op.bv + k + 2);
+      if (c.x >= 0) s = fma(a0.x, u[c.x], s);
+      if (c.y >= 0) s = fma(a0.y, u[c.y], s);
+      if (c.z >= 0) s = fma(a1.x, u[c.z], s);
+      if (c.w >= 0) s = fma(a1.y, u[c.w], s);
+    }
+    const double t = subwarp_sum<L>(s);
+    if (act) {
+      if (FUSE) {
+        const double zr = __dmul_rn(1.0 / dr, rres);
+        if (f.xupd && lane == 0) f.xdst[op.n + r] = __dadd_rn(xs, __dmul_rn(f.alpha_prev, wr));
+        const double pn = f.restart ? zr : __dadd_rn(zr, __dmul_rn(f.beta, wr));
+        if (lane == 0) { w[r] = pn; rzb += rres * zr; }
+        wr = pn;
+      }
+      const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
+      const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
+      if (lane == 0) {
+        y[op.n + r] = yb;
+        acc += t * z + wr * yb;
+        if (CSC) zb[r] = z;
+      }
+      if (!CSC) {
+        if (c0.x >= 0) atomicAdd(y + c0.x, z * v0.x);
+        if (c0.y >= 0) atomicAdd(y + c0.y, z * v0.y);
+        if (c0.z >= 0) atomicAdd(y + c0.z, z * v1.x);
+        if (c0.w >= 0) atomicAdd(y + c0.w, z * v1.y);
+        for (int k = b + 4 * lane + 4 * L; k < e; k += 4 * L) {
+          int4 c = *reinterpret_cast<const int4*>(op.ci + k);
+          double2 a0 = *reinterpret_cast<const double2*>(op.bv + k);
+          double2 a1 = *reinterpret_cast<const double2*>(op.bv + k + 2);
+          if (c.x >= 0) atomicAdd(y + c.x, z * a0.x);
+          if (c.y >= 0) atomicAdd(y + c.y, z * a0.y);
+          if (c.z >= 0) atomicAdd(y + c.z, z * a1.x);
+          if (c.w >= 0) atomicAdd(y + c.w, z * a1.y);
+        }
+      }
+    }
+    r = r1; act = act1; b = b1; e = e1; c0 = cn; v0 = vn0; v1 = vn1;
+    rb1 = rb2; r1 = r2; act1 = act2; b1 = b2; e1 = e2;
+  }
+  *rzb_out = rzb;
+  return acc;
+}
+
+template <int L, bool CSC, bool FUSE, bool PIPE = false>
+__device__ void phase_rows(const Op& op, double* v, double* y, double* zb,
+                           double* part, int G, double* red, double* s_lr, const RowFuse& f) {
+  const double* u = v;
+  double* w = v + op.n;
+  double acc = 0.0, rzb = 0.0;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  if (PIPE) acc = rows_loop_pipelined<L, CSC, FUSE>(op, v, y, zb, f, &rzb);
+  else {
+  const int lane = threadIdx.x & (L - 1);
+  constexpr int RPW = 32 / L;                       // rows per warp step
+  const int sub_in_warp = (threadIdx.x & 31) / L;
+  for (long long rb = (long long)gwarp * RPW; rb < op.m; rb += (long long)nwarp * RPW) {
+    const int r = (int)rb + sub_in_warp;
+    const bool active = r < op.m;
+    int b = 0, e = 0;
+    double dr = 1.0, wr = 0.0;
+    if (active) {
+      b = __ldg(op.rp + r); e = __ldg(op.rp + r + 1);
+      dr = __ldg(op.d + r);
+      wr = w[r];
+      if (FUSE) {
+        // every lane of the row computes the same values; lane 0 stores
+        const double rr = f.r[op.n + r];
+        const double zr = __dmul_rn(1.0 / dr, rr);
+        if (f.xupd && lane == 0) f.xdst[op.n + r] = __dadd_rn(f.xsrc[op.n + r], __dmul_rn(f.alpha_prev, wr));
+        const double pn = f.restart ? zr : __dadd_rn(zr, __dmul_rn(f.beta, wr));
+        if (lane == 0) { w[r] = pn; rzb += rr * zr; }
+        wr = pn;
+      }
+    }
+    const int k0 = b + 4 * lane;
+    int4 c0 = make_int4(-1, -1, -1, -1);
+    double2 v0 = make_double2(0.0, 0.0), v1 = make_double2(0.0, 0.0);
+    if (k0 < e) { c0 = ld_stream_i4(op.ci + k0); v0 = ld_stream_d2(op.bv + k0); v1 = ld_stream_d2(op.bv + k0 + 2); }
+    double s = 0.0;
+    if (c0.x >= 0) s = fma(v0.x, u[c0.x], s);
+    if (c0.y >= 0) s = fma(v0.y, u[c0.y], s);
+    if (c0.z >= 0) s = fma(v1.x, u[c0.z], s);
+    if (c0.w >= 0) s = fma(v1.y, u[c0.w], s);
+#pragma unroll 4
+    for (int k = k0 + 4 * L; k < e; k += 4 * L) {   // rows longer than 4L nonzeros
+      int4 c = ld_stream_i4(op.ci + k);
+      double2 a0 = ld_stream_d2(op.bv + k), a1 = ld_stream_d2(op.bv + k + 2);
+      if (c.x >= 0) s = fma(a0.x, u[c.x], s);
+      if (c.y >= 0) s = fma(a0.y, u[c.y], s);
+      if (c.z >= 0) s = fma(a1.x, u[c.z], s);
+      if (c.w >= 0) s = fma(a1.y, u[c.w], s);
+    }
+    const double t = subwarp_sum<L>(s);
+    if (!active) continue;
+    const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
+    const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
+    if (lane == 0) {
+      y[op.n + r] = yb;
+      acc += t * z + wr * yb;
+      if (CSC) zb[r] = z;
+    }
+    if (!CSC) {
+      if (c0.x >= 0) atomicAdd(y + c0.x, z * v0.x);
+      if (c0.y >= 0) atomicAdd(y + c0.y, z * v0.y);
+      if (c0.z >= 0) atomicAdd(y + c0.z, z * v1.x);
+      if (c0.w >= 0) atomicAdd(y + c0.w, z * v1.y);
+      for (int k = k0 + 4 * L; k < e; k += 4 * L) {
+        int4 c = *reinterpret_cast<const int4*>(op.ci + k);
+        double2 a0 = *reinterpret_cast<const double2*>(op.bv + k);
+        double2 a1 = *reinterpret_cast<const double2*>(op.bv + k + 2);
+        if (c.x >= 0) atomicAdd(y + c.x, z * a0.x);
+        if (c.y >= 0) atomicAdd(y + c.y, z * a0.y);
+        if (c.z >= 0) atomicAdd(y + c.z, z * a1.x);
+        if (c.w >= 0) atomicAdd(y + c.w, z * a1.y);
+      }
+    }
+  }
+  }
+  if (FUSE) {
+    const double t2 = block_sum(rzb, red);
+    if (threadIdx.x == 0) part[SLOT_AUX2 * G + blockIdx.x] = t2;
+  }
+
+  acc += hess_rows(op, u, y, part, G, red, s_lr);
   double tot = block_sum(acc, red);
   if (threadIdx.x == 0) part[SLOT_ROWS * G + blockIdx.x] = tot;
 }

@@ -1,0 +1,549 @@
+// qpk_engine.cuh -- the "slot engine": Jacobi-PCG (linalg.py:66-133) as a
+// sequence of lean kernels instead of one cooperative kernel.
+//
+// One slot = three launches  top -> rows -> update.  A slot is either a PCG
+// iteration (NORMAL / RESTART), the explicit-residual check the reference
+// makes when the recurrence says "converged" (CHECK, linalg.py:112-125), the
+// final true residual of the best iterate at the iteration cap (FINAL,
+// linalg.py:132-133), or empty (DONE).  Which one is decided on the device:
+// the control state lives in HBM, double-buffered by slot parity (slot s
+// reads ctrl[s&1], the last block of its update kernel writes ctrl[(s+1)&1]),
+// so the host only enqueues identical slots (replayed as a CUDA graph) and
+// polls for DONE every few slots.  Each kernel has its own launch bounds, and
+// the multi-GPU path inserts its collectives between the kernels of a slot.
+#pragma once
+#include "qpk_device.cuh"
+
+#ifndef QPK_ROWS_PIPE
+#define QPK_ROWS_PIPE true
+#endif
+#ifndef QPK_ROWS_MINB
+#define QPK_ROWS_MINB 4
+#endif
+
+namespace qpk {
+
+enum { MODE_NORMAL = 0, MODE_RESTART = 1, MODE_CHECK = 2, MODE_FINAL = 3, MODE_DONE = 4 };
+
+struct Ctrl {
+  int mode, k, cur, best, xn, xupd, status, converged, restarts, applies, result, pad;
+  double rz, rnorm, best_rnorm, thr, rhs_norm, alpha_prev, beta, final_norm;
+  unsigned long long t_top, t_rows, t_upd, ph[4];
+};
+
+struct EngineCfg {
+  double tol;
+  long long max_iters;
+  int rel;
+  int pad;
+  double* hist;       // nullable, max_iters + 1
+};
+
+#ifndef QPK_DICT_MAX
+#define QPK_DICT_MAX 1024        // distinct columns per row block
+#endif
+#define QPK_DICT_WARPS 8         // warps per CTA in the dictionary kernels
+#define QPK_DICT_ROWS 512        // rows per block (at most)
+
+// Row-block dictionaries: rows [blk_row[b], blk_row[b+1]) touch the sorted
+// global columns cols[blk_dict[b] .. blk_dict[b+1]); lci holds each B entry's
+// index into its block's dictionary (0xFFFF = padding).  bpart[p] is block b's
+// partial of (B'z) for dictionary position p; col_pos[col_ptr[j] ..
+// col_ptr[j+1]) lists column j's positions in block order.
+struct Dict {
+  int nblk;
+  const int* blk_row;
+  const int* blk_dict;
+  const int* cols;
+  const unsigned short* lci;
+  double* bpart;
+  const int* col_ptr;
+  const int* col_pos;
+};
+
+struct Engine {
+  Op op;
+  Dict dict;
+  int scatter;                // 1 atomic, 2 CSC segments, 3 row-block dictionary
+  const int* seg_ptr;         // CSC segments: column j owns segments [seg_ptr[j], seg_ptr[j+1])
+  const int* seg_beg;         // segment q covers padded CSC entries [seg_beg[q], seg_beg[q+1])
+  double* seg_sum;            // per-segment partial of (B'z)
+  int n_seg;
+  int seg_lanes;              // lanes per segment (segment <= 8 * seg_lanes entries)
+  const double* rhs;
+  double* x[3];
+  double* r; double* p; double* y; double* zb;
+  const double* minv;
+  double* part; int G;
+  Ctrl* ctrl;                 // [2]
+  unsigned int* counter;      // last-block ticket
+  const EngineCfg* cfg;
+};
+
+__device__ __forceinline__ int spare_of(int cur, int best) {
+  return (cur != best) ? 3 - cur - best : (cur + 1) % 3;
+}
+
+// Last-block-done: every block has written its partials; the block that takes
+// the final ticket sees all of them.  Returns true in exactly one block.
+__device__ __forceinline__ bool last_block(unsigned int* counter) {
+  __shared__ bool am_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) am_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *counter = 0u;
+  }
+  return am_last;
+}
+
+// ----------------------------------------------------------------- init ----
+// x0 = 0, r = rhs (linalg.py:85-87); last block: ||rhs||, threshold
+// (linalg.py:83), early return when rnorm <= threshold (linalg.py:93-94).
+__global__ void __launch_bounds__(QPK_BLOCK) k_engine_init(Engine E) {
+  __shared__ double red[32];
+  const int N = E.op.n + E.op.m;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const double b = __ldg(E.rhs + i);
+    E.x[0][i] = 0.0;
+    E.r[i] = b;
+    acc += b * b;
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) E.part[SLOT_AUX * E.G + blockIdx.x] = t;
+  if (!last_block(E.counter)) return;
+  const double rn = sqrt(grid_total(E.part + SLOT_AUX * E.G, E.G, red));
+  if (threadIdx.x == 0) {
+    const EngineCfg cfg = *E.cfg;
+    Ctrl c;
+    memset(&c, 0, sizeof c);
+    c.rhs_norm = rn;
+    c.thr = cfg.rel ? cfg.tol * rn : cfg.tol;
+    c.rnorm = rn;
+    c.best_rnorm = rn;
+    c.mode = (rn <= c.thr) ? MODE_DONE : MODE_RESTART;
+    c.converged = rn <= c.thr;
+    c.final_norm = rn;
+    c.t_top = globaltimer_ns();
+    if (cfg.hist) cfg.hist[0] = rn;
+    E.ctrl[0] = c;
+  }
+}
+
+// ------------------------------------------------------------------ top ----
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
+  __shared__ double red[32];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_top = globaltimer_ns();
+  const Op& op = E.op;
+  const int N = op.n + op.m, G = E.G;
+  double rz = 0.0, acc = 0.0;
+  double sacc[QPK_KMAX];
+  const bool lr = op.H.kind == HESS_LOWRANK;
+  if (lr) for (int kk = 0; kk < op.H.k; ++kk) sacc[kk] = 0.0;
+  if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
+    // x_t += alpha_prev p_t (lazy), z = M^-1 r, p_t = z (+ beta p_t), y_t = diag(Q) p_t
+    const bool restart = c.mode == MODE_RESTART;
+    const double* xs = E.x[c.cur];
+    double* xd = E.x[c.xn];
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < op.n; j += gridDim.x * blockDim.x) {
+      const double pold = E.p[j];
+      if (c.xupd) xd[j] = __dadd_rn(xs[j], __dmul_rn(c.alpha_prev, pold));
+      const double rj = E.r[j];
+      const double zj = __dmul_rn(__ldg(E.minv + j), rj);
+      rz += rj * zj;
+      const double pn = restart ? zj : __dadd_rn(zj, __dmul_rn(c.beta, pold));
+      E.p[j] = pn;
+      acc += prep_elem(op, j, pn, E.y);
+      if (lr) lowrank_accum(op, j, pn, sacc);
+    }
+  } else {
+    // CHECK: materialise the pending x_k into x[xn] and prep(x_k).
+    // FINAL: materialise the pending x (if any) and prep(x_best).
+    const int target = (c.mode == MODE_CHECK) ? c.xn : c.best;
+    const double* xs = E.x[c.cur];
+    double* xd = E.x[c.xn];
+    const double* xt = E.x[target];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+      double xv = 0.0;
+      if (c.xupd) { xv = __dadd_rn(xs[i], __dmul_rn(c.alpha_prev, E.p[i])); xd[i] = xv; }
+      if (i < op.n) {
+        const double v = (c.xupd && target == c.xn) ? xv : xt[i];
+        acc += prep_elem(op, i, v, E.y);
+        if (lr) lowrank_accum(op, i, v, sacc);
+      }
+    }
+  }
+  double t = block_sum(rz, red);
+  if (threadIdx.x == 0) E.part[SLOT_AUX * G + blockIdx.x] = t;
+  t = block_sum(acc, red);
+  if (threadIdx.x == 0) E.part[SLOT_PREP * G + blockIdx.x] = t;
+  if (lr) lowrank_flush(op, sacc, E.part, G, red);
+}
+
+// ----------------------------------------------------------------- rows ----
+template <int L, bool CSC>
+__global__ void __launch_bounds__(QPK_BLOCK, QPK_ROWS_MINB) k_slot_rows(Engine E, int par) {
+  __shared__ double red[32];
+  __shared__ double s_lr[QPK_KMAX];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_rows = globaltimer_ns();
+  if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
+    RowFuse f;
+    f.r = E.r;
+    f.xsrc = E.x[c.cur];
+    f.xdst = E.x[c.xn];
+    f.alpha_prev = c.alpha_prev;
+    f.beta = c.beta;
+    f.restart = c.mode == MODE_RESTART;
+    f.xupd = c.xupd;
+    phase_rows<L, CSC, true, QPK_ROWS_PIPE>(E.op, E.p, E.y, E.zb, E.part, E.G, red, s_lr, f);
+  } else {
+    RowFuse none{};
+    double* v = E.x[c.mode == MODE_CHECK ? c.xn : c.best];
+    phase_rows<L, CSC, false, QPK_ROWS_PIPE>(E.op, v, E.y, E.zb, E.part, E.G, red, s_lr, none);
+  }
+}
+
+// ------------------------------------------------------------------ csc ----
+// B'z by column segments (deterministic, no atomics): each group of LS lanes
+// owns one segment of <= 8 LS entries, so every lane issues its two chunks of
+// row indices / values and all 8 z gathers at once.  Long columns (the dense
+// X block of cfg2, RT bands) are split over many groups; short ones fill one.
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_csc(Engine E, int par) {
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  const Op& op = E.op;
+  const int LS = E.seg_lanes;
+  const int ls = threadIdx.x & (LS - 1);
+  const int per = 32 / LS, sw = (threadIdx.x & 31) / LS;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarp = (gridDim.x * blockDim.x) >> 5;
+  const double* zb = E.zb;
+  for (long long qb = (long long)gwarp * per; qb < E.n_seg; qb += (long long)nwarp * per) {
+    const int q = (int)qb + sw;
+    double s0 = 0.0, s1 = 0.0;
+    if (q < E.n_seg) {
+      const int b = __ldg(E.seg_beg + q), e = __ldg(E.seg_beg + q + 1);
+      const int k = b + 4 * ls, k2 = k + 4 * LS;
+      int4 c0 = make_int4(-1, -1, -1, -1), c1 = c0;
+      double2 a0 = make_double2(0.0, 0.0), a1 = a0, b0 = a0, b1 = a0;
+      if (k < e) { c0 = ld_stream_i4(op.ri + k); a0 = ld_stream_d2(op.cv + k); a1 = ld_stream_d2(op.cv + k + 2); }
+      if (k2 < e) { c1 = ld_stream_i4(op.ri + k2); b0 = ld_stream_d2(op.cv + k2); b1 = ld_stream_d2(op.cv + k2 + 2); }
+      if (c0.x >= 0) s0 = fma(a0.x, zb[c0.x], s0);
+      if (c0.y >= 0) s0 = fma(a0.y, zb[c0.y], s0);
+      if (c0.z >= 0) s0 = fma(a1.x, zb[c0.z], s0);
+      if (c0.w >= 0) s0 = fma(a1.y, zb[c0.w], s0);
+      if (c1.x >= 0) s1 = fma(b0.x, zb[c1.x], s1);
+      if (c1.y >= 0) s1 = fma(b0.y, zb[c1.y], s1);
+      if (c1.z >= 0) s1 = fma(b1.x, zb[c1.z], s1);
+      if (c1.w >= 0) s1 = fma(b1.y, zb[c1.w], s1);
+    }
+    double s = s0 + s1;
+    for (int o = LS / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (q < E.n_seg && ls == 0) E.seg_sum[q] = s;
+  }
+}
+
+// y_j (final) of a top entry: y_j plus its column's deterministic partials
+// (CSC segments, or dictionary block partials), summed in a fixed order
+template <int SC>
+__device__ __forceinline__ double top_value(const Engine& E, int j) {
+  double s = 0.0;
+  if (SC == 2) {
+    const int qb = __ldg(E.seg_ptr + j), qe = __ldg(E.seg_ptr + j + 1);
+    for (int q = qb; q < qe; ++q) s += E.seg_sum[q];
+  } else if (SC == 3) {
+    const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
+    for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
+  }
+  return E.y[j] + s;
+}
+
+// ------------------------------------------------------------- dictionary ----
+// One pass over B with no atomics: a CTA takes a row block, stages u[dict]
+// in shared memory, and each warp processes one row at a time (32 lanes,
+// distinct columns), gathering u from shared memory and accumulating z B_r
+// into its own shared-memory copy of the block's dictionary.  The 8 copies
+// are summed in a fixed order into bpart (one value per block and column).
+template <int MODE_JAC>
+__device__ __forceinline__ void dict_rows(const Engine& E, double* v, const RowFuse& f, bool fuse,
+                                          double* sm, double& pacc, double& rzb) {
+  const Op& op = E.op;
+  const Dict& D = E.dict;
+  const double* u = v;
+  double* w = v + op.n;
+  double* us = sm;
+  double* acc = sm + QPK_DICT_MAX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* aw = acc + warp * QPK_DICT_MAX;
+  for (int blk = blockIdx.x; blk < D.nblk; blk += gridDim.x) {
+    const int r0 = __ldg(D.blk_row + blk), r1 = __ldg(D.blk_row + blk + 1);
+    const int d0 = __ldg(D.blk_dict + blk), nd = __ldg(D.blk_dict + blk + 1) - d0;
+    for (int k = threadIdx.x; k < nd; k += blockDim.x) {
+      if (!MODE_JAC) us[k] = u[__ldg(D.cols + d0 + k)];
+#pragma unroll
+      for (int ww = 0; ww < QPK_DICT_WARPS; ++ww) acc[ww * QPK_DICT_MAX + k] = 0.0;
+    }
+    __syncthreads();
+    for (int r = r0 + warp; r < r1; r += QPK_DICT_WARPS) {
+      const int b = __ldg(op.rp + r), e = __ldg(op.rp + r + 1);
+      const double dr = __ldg(op.d + r);
+      unsigned short li[4];
+      double vv[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = b + lane + 32 * q;
+        li[q] = 0xFFFF;
+        vv[q] = 0.0;
+        if (k < e) { li[q] = __ldg(D.lci + k); vv[q] = __ldg(op.bv + k); }
+      }
+      double z;
+      if (MODE_JAC) {
+        z = 1.0 / dr;                                   // Jacobi: sum_r B_rj^2 / d_r
+      } else {
+        double wr = w[r];
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) if (li[q] != 0xFFFF) s = fma(vv[q], us[li[q]], s);
+        for (int k = b + lane + 128; k < e; k += 32) {
+          const unsigned short l = __ldg(D.lci + k);
+          if (l != 0xFFFF) s = fma(__ldg(op.bv + k), us[l], s);
+        }
+        const double t = subwarp_sum<32>(s);
+        if (fuse) {
+          const double rres = f.r[op.n + r];
+          const double zr = __dmul_rn(1.0 / dr, rres);
+          if (f.xupd && lane == 0) f.xdst[op.n + r] = __dadd_rn(f.xsrc[op.n + r], __dmul_rn(f.alpha_prev, wr));
+          const double pn = f.restart ? zr : __dadd_rn(zr, __dmul_rn(f.beta, wr));
+          if (lane == 0) { w[r] = pn; rzb += rres * zr; }
+          wr = pn;
+        }
+        z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
+        const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
+        if (lane == 0) {
+          E.y[op.n + r] = yb;
+          pacc += t * z + wr * yb;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (li[q] != 0xFFFF) aw[li[q]] += MODE_JAC ? __dmul_rn(vv[q], vv[q]) * z : z * vv[q];
+      for (int k = b + lane + 128; k < e; k += 32) {
+        const unsigned short l = __ldg(D.lci + k);
+        if (l != 0xFFFF) {
+          const double a = __ldg(op.bv + k);
+          aw[l] += MODE_JAC ? __dmul_rn(a, a) * z : z * a;
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < nd; k += blockDim.x) {
+      double s = 0.0;
+#pragma unroll
+      for (int ww = 0; ww < QPK_DICT_WARPS; ++ww) s += acc[ww * QPK_DICT_MAX + k];
+      D.bpart[d0 + k] = s;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(QPK_DICT_WARPS * 32, 3) k_slot_rows_dict(Engine E, int par) {
+  extern __shared__ double sm[];
+  __shared__ double red[32];
+  __shared__ double s_lr[QPK_KMAX];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_rows = globaltimer_ns();
+  const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
+  RowFuse f{};
+  double* v;
+  if (fuse) {
+    f.r = E.r; f.xsrc = E.x[c.cur]; f.xdst = E.x[c.xn];
+    f.alpha_prev = c.alpha_prev; f.beta = c.beta;
+    f.restart = c.mode == MODE_RESTART; f.xupd = c.xupd;
+    v = E.p;
+  } else {
+    v = E.x[c.mode == MODE_CHECK ? c.xn : c.best];
+  }
+  double pacc = 0.0, rzb = 0.0;
+  dict_rows<0>(E, v, f, fuse, sm, pacc, rzb);
+  pacc += hess_rows(E.op, v, E.y, E.part, E.G, red, s_lr);
+  double t = block_sum(pacc, red);
+  if (threadIdx.x == 0) E.part[SLOT_ROWS * E.G + blockIdx.x] = t;
+  t = block_sum(rzb, red);
+  if (threadIdx.x == 0) E.part[SLOT_AUX2 * E.G + blockIdx.x] = t;
+}
+
+// Jacobi through the dictionaries (deterministic): bpart <- sum_r B_rj^2 / d_r
+__global__ void __launch_bounds__(QPK_DICT_WARPS * 32, 3) k_jac_dict(Engine E) {
+  extern __shared__ double sm[];
+  RowFuse f{};
+  double pacc = 0.0, rzb = 0.0;
+  dict_rows<1>(E, nullptr, f, false, sm, pacc, rzb);
+}
+
+// jac_top = (diag(H) + q) + 2 sum of the column's partials ; bottom = D
+__global__ void k_jac_dict_finish(Engine E, const double* hdiag, double* jac, double* minv) {
+  const Op& op = E.op;
+  const int N = op.n + op.m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    double v;
+    if (i < op.n) {
+      double s = 0.0;
+      const int qb = __ldg(E.dict.col_ptr + i), qe = __ldg(E.dict.col_ptr + i + 1);
+      for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
+      v = __dadd_rn(__dadd_rn(__ldg(hdiag + i), __ldg(op.q + i)), __dmul_rn(2.0, s));
+    } else {
+      v = __ldg(op.d + (i - op.n));
+    }
+    jac[i] = v;
+    minv[i] = 1.0 / v;
+  }
+}
+
+// --------------------------------------------------------------- update ----
+template <int SC>
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
+  constexpr bool CSC = SC != 1;
+  __shared__ double red[32];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par ^ 1] = c;
+    return;
+  }
+  const unsigned long long t_upd = globaltimer_ns();
+  const Op& op = E.op;
+  const int G = E.G;
+  const int N = op.n + op.m;
+  double rr = 0.0, rzn = 0.0;
+  double alpha = 0.0, rz = c.rz;
+  if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
+    const double pap = grid_total(E.part + SLOT_ROWS * G, G, red) + grid_total(E.part + SLOT_PREP * G, G, red);
+    if (c.mode == MODE_RESTART)
+      rz = grid_total(E.part + SLOT_AUX * G, G, red) + grid_total(E.part + SLOT_AUX2 * G, G, red);
+    if (pap <= 0.0) {                                                   // linalg.py:102-103
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Ctrl o = c;
+        o.mode = MODE_DONE;
+        o.status = QPK_PCG_BREAKDOWN;
+        o.converged = 0;
+        o.applies += 1;
+        o.final_norm = c.best_rnorm;
+        o.result = c.best;
+        E.ctrl[par ^ 1] = o;
+      }
+      return;
+    }
+    alpha = rz / pap;
+    if (!CSC) {
+      const int np = N >> 1;
+      double2* r2 = reinterpret_cast<double2*>(E.r);
+      const double2* y2 = reinterpret_cast<const double2*>(E.y);
+      const double2* m2 = reinterpret_cast<const double2*>(E.minv);
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+        double2 ri = r2[i];
+        const double2 yi = y2[i];
+        const double2 mi = __ldg(m2 + i);
+        ri.x = __dsub_rn(ri.x, __dmul_rn(alpha, yi.x));
+        ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yi.y));
+        r2[i] = ri;
+        rr += ri.x * ri.x + ri.y * ri.y;
+        rzn += ri.x * __dmul_rn(mi.x, ri.x) + ri.y * __dmul_rn(mi.y, ri.y);
+      }
+      if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
+        E.r[N - 1] = ri;
+        rr += ri * ri;
+        rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
+      }
+    } else {
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
+        const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
+        E.r[i] = ri;
+        rr += ri * ri;
+        rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
+      }
+    }
+  } else {
+    // explicit residual rhs - K x (CHECK stores it as the new r; FINAL only needs its norm)
+    const bool store = c.mode == MODE_CHECK;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+      const double yi = (CSC && i < op.n) ? top_value<SC>(E, i) : E.y[i];
+      const double ri = __dsub_rn(__ldg(E.rhs + i), yi);
+      if (store) E.r[i] = ri;
+      rr += ri * ri;
+    }
+  }
+  double t = block_sum(rr, red);
+  if (threadIdx.x == 0) E.part[SLOT_RR * G + blockIdx.x] = t;
+  t = block_sum(rzn, red);
+  if (threadIdx.x == 0) E.part[SLOT_RZ * G + blockIdx.x] = t;
+  if (!last_block(E.counter)) return;
+
+  // ---- decision (one block) ----
+  const double rr_tot = grid_total(E.part + SLOT_RR * G, G, red);
+  const double rz_tot = grid_total(E.part + SLOT_RZ * G, G, red);
+  if (threadIdx.x != 0) return;
+  const EngineCfg cfg = *E.cfg;
+  const unsigned long long now = globaltimer_ns();
+  Ctrl o = c;
+  o.applies += 1;
+  o.ph[0] += c.t_rows - c.t_top;
+  o.ph[1] += t_upd - c.t_rows;
+  o.ph[2] += now - t_upd;
+  const double nrm = sqrt(rr_tot);
+  if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
+    const int cur = c.xupd ? c.xn : c.cur;               // x_{k-1} was materialised this slot
+    o.k = c.k + 1;
+    if (cfg.hist) cfg.hist[o.k] = nrm;
+    o.rnorm = nrm;
+    o.cur = cur;
+    o.xn = spare_of(cur, c.best);                        // x_k = x_{k-1} + alpha p lands here
+    o.xupd = 1;
+    o.alpha_prev = alpha;
+    if (nrm < c.best_rnorm) { o.best = o.xn; o.best_rnorm = nrm; }   // linalg.py:110-111
+    if (nrm <= c.thr) {
+      o.mode = MODE_CHECK;                                // linalg.py:112
+    } else if (o.k >= cfg.max_iters) {
+      o.mode = MODE_FINAL;
+    } else {
+      o.mode = MODE_NORMAL;                               // linalg.py:126-130
+      o.beta = rz_tot / rz;
+      o.rz = rz_tot;
+    }
+  } else if (c.mode == MODE_CHECK) {
+    o.cur = c.xn;
+    o.xupd = 0;
+    if (nrm <= c.thr) {                                   // linalg.py:115-116
+      o.mode = MODE_DONE;
+      o.converged = 1;
+      o.final_norm = nrm;
+      o.result = c.xn;
+    } else {                                              // linalg.py:117-125
+      o.restarts += 1;
+      o.rnorm = nrm;
+      if (nrm < c.best_rnorm) { o.best = c.xn; o.best_rnorm = nrm; }
+      o.xn = spare_of(o.cur, o.best);
+      o.mode = (c.k >= cfg.max_iters) ? MODE_FINAL : MODE_RESTART;
+    }
+  } else {                                                // FINAL (linalg.py:132-133)
+    o.mode = MODE_DONE;
+    o.k = (int)cfg.max_iters;
+    o.converged = nrm <= c.thr;
+    o.final_norm = nrm;
+    o.result = c.best;
+    o.cur = c.xupd ? c.xn : c.cur;
+    o.xupd = 0;
+  }
+  E.ctrl[par ^ 1] = o;
+}
+
+}  // namespace qpk

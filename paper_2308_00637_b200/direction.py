@@ -58,8 +58,7 @@ class GpuKkt:
                     c.call("qpk_problem_add_rows", int(am.n_rows), _native.ptr(ro), _native.ptr(ci),
                            _native.ptr(v), _native.ptr(rows), len(rows), sign)
         self._set_hessian(problem.hessian)
-        if scatter == _native.QPK_SCATTER_AUTO:
-            scatter = int(os.environ.get("QPK_SCATTER", _native.QPK_SCATTER_ATOMIC))
+        # AUTO lets the library pick per matrix (QPK_SCATTER in the environment overrides)
         c.call("qpk_problem_finalize", int(scatter))
         self._hist = None
 
