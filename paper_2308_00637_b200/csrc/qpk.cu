@@ -25,6 +25,7 @@
 #include "../../include/qpk.h"
 #include "qpk_device.cuh"
 #include "qpk_engine.cuh"
+#include "qpk_tma.cuh"
 
 namespace cg = cooperative_groups;
 using namespace qpk;
@@ -447,7 +448,8 @@ struct qpk_ctx {
   DBuf<double> seg_sum;
   int n_seg = 0, seg_lanes = 8;
   // row-block dictionaries
-  DBuf<int> blk_row, blk_dict, dcols, col_ptr, col_pos;
+  DBuf<int> blk_row, blk_dict, dcols, col_ptr, col_pos, tile_row, blk_tile;
+  DBuf<int4> tile_desc;
   DBuf<unsigned short> lci;
   DBuf<double> bpart;
   int nblk = 0;
@@ -778,6 +780,20 @@ static int build_dict(qpk_ctx* c) {
     ++rows_in;
   }
   if (rows_in > 0) close_block(m);
+  // tiles for the TMA pipeline: <= QPK_TILE_E padded entries and <= QPK_TILE_R rows
+  std::vector<int> tile_row, blk_tile(1, 0);
+  for (int b = 0; b < blk; ++b) {
+    int r = blk_row[b];
+    while (r < blk_row[b + 1]) {
+      tile_row.push_back(r);
+      int rows = 0;
+      const int e0 = c->h_rp[r];
+      while (r < blk_row[b + 1] && rows < QPK_TILE_R && c->h_rp[r + 1] - e0 <= QPK_TILE_E - 16) { ++r; ++rows; }
+      if (rows == 0) return QPK_OK;                          // a row wider than a tile
+    }
+    blk_tile.push_back((int)tile_row.size());
+  }
+  tile_row.push_back((int)m);
   // column -> its dictionary positions, in block order
   std::vector<int> col_ptr(n + 1, 0), col_pos(cols.size());
   for (int col : cols) col_ptr[col + 1]++;
@@ -790,9 +806,22 @@ static int build_dict(qpk_ctx* c) {
   CUDA_TRY(upload(c->blk_row, blk_row, s));
   CUDA_TRY(upload(c->blk_dict, blk_dict, s));
   CUDA_TRY(upload(c->dcols, cols, s));
-  CUDA_TRY(upload(c->lci, lci, s));
   CUDA_TRY(upload(c->col_ptr, col_ptr, s));
   CUDA_TRY(upload(c->col_pos, col_pos, s));
+  CUDA_TRY(upload(c->tile_row, tile_row, s));
+  CUDA_TRY(upload(c->blk_tile, blk_tile, s));
+  {
+    std::vector<int4> td(tile_row.size() - 1);
+    for (size_t t = 0; t + 1 < tile_row.size(); ++t)
+      td[t] = make_int4(tile_row[t], tile_row[t + 1], c->h_rp[tile_row[t]], c->h_rp[tile_row[t + 1]]);
+    CUDA_TRY(upload(c->tile_desc, td, s));
+  }
+  {
+    // bulk copies may over-read a few aligned elements past the end
+    std::vector<unsigned short> pad = lci;
+    pad.resize(lci.size() + 32, 0xFFFF);
+    CUDA_TRY(upload(c->lci, pad, s));
+  }
   CUDA_TRY(c->bpart.alloc(std::max<size_t>(cols.size(), 1)));
   CUDA_TRY(cudaStreamSynchronize(s));
   c->nblk = blk;
@@ -808,9 +837,18 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   if (c->hkind < 0) return fail(QPK_E_STATE, "qpk_problem_finalize: Hessian not set");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
-  CUDA_TRY(upload(c->rp, c->h_rp, s));
-  CUDA_TRY(upload(c->ci, c->h_ci, s));
-  CUDA_TRY(upload(c->bv, c->h_v, s));
+  {
+    // pad: the TMA tiles read aligned windows that may extend past the end
+    std::vector<int> rp = c->h_rp;
+    rp.resize(rp.size() + 16, rp.back());
+    CUDA_TRY(upload(c->rp, rp, s));
+    std::vector<int> ci = c->h_ci;
+    ci.resize(ci.size() + 32, -1);
+    CUDA_TRY(upload(c->ci, ci, s));
+    std::vector<double> bv = c->h_v;
+    bv.resize(bv.size() + 32, 0.0);
+    CUDA_TRY(upload(c->bv, bv, s));
+  }
   if (c->hkind == QPK_HESS_DIAG || c->hkind == QPK_HESS_LOWRANK) CUDA_TRY(upload(c->hh, c->h_h, s));
   if (c->hkind == QPK_HESS_CSR) {
     CUDA_TRY(upload(c->hrp, c->h_hrp, s));
@@ -824,16 +862,16 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   }
   const long long N = c->N();
   CUDA_TRY(c->hdiag.alloc(c->n));
-  CUDA_TRY(c->d.alloc(std::max<long long>(c->m, 1)));
+  CUDA_TRY(c->d.alloc(c->m + 8));
   CUDA_TRY(c->q.alloc(c->n));
   CUDA_TRY(c->jac.alloc(N));
   CUDA_TRY(c->minv.alloc(N));
-  for (auto& b : c->x) CUDA_TRY(b.alloc(N));
-  CUDA_TRY(c->r.alloc(N));
-  CUDA_TRY(c->p.alloc(N));
-  CUDA_TRY(c->y.alloc(N));
-  CUDA_TRY(c->rhs.alloc(N));
-  CUDA_TRY(c->vin.alloc(N));
+  for (auto& b : c->x) CUDA_TRY(b.alloc(N + 8));
+  CUDA_TRY(c->r.alloc(N + 8));
+  CUDA_TRY(c->p.alloc(N + 8));
+  CUDA_TRY(c->y.alloc(N + 8));
+  CUDA_TRY(c->rhs.alloc(N + 8));
+  CUDA_TRY(c->vin.alloc(N + 8));
   CUDA_TRY(c->zb.alloc(std::max<long long>(c->m, 1)));
 
   // lanes per row: ~3 chunks of 4 nonzeros per lane keeps several gathers in flight
@@ -996,7 +1034,11 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   const int G = c->grid_eng;
   k_slot_top<<<G, QPK_BLOCK, 0, s>>>(E, par);
   if (c->scatter == QPK_SCATTER_DICT) {
-    k_slot_rows_dict<<<G, QPK_DICT_WARPS * 32, DICT_SMEM, s>>>(E, par);
+    Tiles T;
+    T.tile_row = c->tile_row.p;
+    T.blk_tile = c->blk_tile.p;
+    T.tile_desc = c->tile_desc.p;
+    k_slot_rows_tma<<<E.G_rows, (QPK_DICT_WARPS + 1) * 32, sizeof(TmaSmem), s>>>(E, T, par);
     k_slot_update<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
     return;
   }
@@ -1028,6 +1070,7 @@ static Engine make_engine(qpk_ctx* c) {
   for (int i = 0; i < 3; ++i) E.x[i] = c->x[i].p;
   E.r = c->r.p; E.p = c->p.p; E.y = c->y.p; E.zb = c->zb.p; E.minv = c->minv.p;
   E.part = c->part.p; E.G = c->grid_eng;
+  E.G_rows = (c->scatter == QPK_SCATTER_DICT) ? std::min(c->sms, c->grid_eng) : c->grid_eng;
   E.ctrl = c->ctrl.p; E.counter = c->counter.p; E.cfg = c->ecfg.p;
   E.seg_ptr = c->seg_ptr.p; E.seg_beg = c->seg_beg.p; E.seg_sum = c->seg_sum.p;
   E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
@@ -1041,6 +1084,7 @@ static int engine_setup(qpk_ctx* c) {
   if (c->ctrl.p) return QPK_OK;
   CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(k_jac_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
+  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TmaSmem)));
   CUDA_TRY(c->ctrl.alloc(2));
   CUDA_TRY(c->counter.alloc(1));
   CUDA_TRY(c->ecfg.alloc(1));

@@ -15,7 +15,7 @@
 #include "qpk_device.cuh"
 
 #ifndef QPK_ROWS_PIPE
-#define QPK_ROWS_PIPE true
+#define QPK_ROWS_PIPE false
 #endif
 #ifndef QPK_ROWS_MINB
 #define QPK_ROWS_MINB 4
@@ -75,6 +75,7 @@ struct Engine {
   double* r; double* p; double* y; double* zb;
   const double* minv;
   double* part; int G;
+  int G_rows;                 // blocks of the rows kernel (its partials; <= G)
   Ctrl* ctrl;                 // [2]
   unsigned int* counter;      // last-block ticket
   const EngineCfg* cfg;
@@ -425,9 +426,9 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
   double rr = 0.0, rzn = 0.0;
   double alpha = 0.0, rz = c.rz;
   if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
-    const double pap = grid_total(E.part + SLOT_ROWS * G, G, red) + grid_total(E.part + SLOT_PREP * G, G, red);
+    const double pap = grid_total(E.part + SLOT_ROWS * G, E.G_rows, red) + grid_total(E.part + SLOT_PREP * G, G, red);
     if (c.mode == MODE_RESTART)
-      rz = grid_total(E.part + SLOT_AUX * G, G, red) + grid_total(E.part + SLOT_AUX2 * G, G, red);
+      rz = grid_total(E.part + SLOT_AUX * G, G, red) + grid_total(E.part + SLOT_AUX2 * G, E.G_rows, red);
     if (pap <= 0.0) {                                                   // linalg.py:102-103
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         Ctrl o = c;
