@@ -449,7 +449,9 @@ struct qpk_ctx {
   int n_seg = 0, seg_lanes = 8;
   // row-block dictionaries
   DBuf<int> blk_row, blk_dict, dcols, col_ptr, col_pos, tile_row, blk_tile;
-  DBuf<int4> tile_desc;
+  DBuf<int4> tile_desc, rtile_desc;
+  int n_rtiles = 0;
+  int tma_rows = -1;              // -1 auto (env QPK_TMA_ROWS)
   DBuf<unsigned short> lci;
   DBuf<double> bpart;
   int nblk = 0;
@@ -875,8 +877,23 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   CUDA_TRY(c->zb.alloc(std::max<long long>(c->m, 1)));
 
   // lanes per row: ~3 chunks of 4 nonzeros per lane keeps several gathers in flight
-  c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 12, 1, 32);
+  c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 12, 4, 32);
   if (const char* ev = getenv("QPK_LANES")) c->lanes = pow2_clamp(atoi(ev), 1, 32);
+  {
+    // flat row tiles for the TMA-fed CSR rows kernel
+    std::vector<int4> rt;
+    long long r = 0;
+    while (r < c->m) {
+      const long long ra = r;
+      const int e0 = c->h_rp[r];
+      int rows = 0;
+      while (r < c->m && rows < QPK_TILE_R && c->h_rp[r + 1] - e0 <= QPK_TILE_E - 8) { ++r; ++rows; }
+      if (rows == 0) { rt.clear(); break; }         // a row wider than a tile: no TMA rows path
+      rt.push_back(make_int4((int)ra, (int)r, c->h_rp[ra], c->h_rp[r]));
+    }
+    c->n_rtiles = (int)rt.size();
+    if (c->n_rtiles) CUDA_TRY(upload(c->rtile_desc, rt, s));
+  }
   // B'z strategy.  AUTO: the row-block dictionary when blocks reuse their
   // columns (banded / clustered B: RT, SVM, dense), else one-pass atomics
   // (random B, where no blocking creates reuse).  CSC and DICT are
@@ -1024,8 +1041,26 @@ int qpk_apply_dev(qpk_ctx* c, const double* v, double* y) {
 }  // extern "C"
 
 // ------------------------------------------------------------ slot engine ---
+static bool use_tma_rows(const qpk_ctx* c) {
+  if (c->n_rtiles <= 0) return false;
+  if (c->tma_rows >= 0) return c->tma_rows == 1;
+  const char* ev = getenv("QPK_TMA_ROWS");           // experimental: off unless asked for
+  return ev ? atoi(ev) == 1 : false;
+}
+
 template <int L, bool CSC>
-static void launch_slot_rows_t(int grid, cudaStream_t s, const Engine& E, int par) {
+static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const Engine& E, int par) {
+  if (use_tma_rows(c)) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_slot_rows_tma_csr<L, CSC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)sizeof(CsrSmem));
+      attr = true;
+    }
+    k_slot_rows_tma_csr<L, CSC><<<E.G_rows, (QPK_CSR_WARPS + 1) * 32, sizeof(CsrSmem), s>>>(E, c->rtile_desc.p,
+                                                                                          c->n_rtiles, par);
+    return;
+  }
   k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
 }
 
@@ -1043,18 +1078,18 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
     return;
   }
   switch (c->lanes * 2 + (csc ? 1 : 0)) {
-    case 2: launch_slot_rows_t<1, false>(G, s, E, par); break;
-    case 3: launch_slot_rows_t<1, true>(G, s, E, par); break;
-    case 4: launch_slot_rows_t<2, false>(G, s, E, par); break;
-    case 5: launch_slot_rows_t<2, true>(G, s, E, par); break;
-    case 8: launch_slot_rows_t<4, false>(G, s, E, par); break;
-    case 9: launch_slot_rows_t<4, true>(G, s, E, par); break;
-    case 16: launch_slot_rows_t<8, false>(G, s, E, par); break;
-    case 17: launch_slot_rows_t<8, true>(G, s, E, par); break;
-    case 32: launch_slot_rows_t<16, false>(G, s, E, par); break;
-    case 33: launch_slot_rows_t<16, true>(G, s, E, par); break;
-    case 64: launch_slot_rows_t<32, false>(G, s, E, par); break;
-    default: launch_slot_rows_t<32, true>(G, s, E, par); break;
+    case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
+    case 3: launch_slot_rows_t<1, true>(c, G, s, E, par); break;
+    case 4: launch_slot_rows_t<2, false>(c, G, s, E, par); break;
+    case 5: launch_slot_rows_t<2, true>(c, G, s, E, par); break;
+    case 8: launch_slot_rows_t<4, false>(c, G, s, E, par); break;
+    case 9: launch_slot_rows_t<4, true>(c, G, s, E, par); break;
+    case 16: launch_slot_rows_t<8, false>(c, G, s, E, par); break;
+    case 17: launch_slot_rows_t<8, true>(c, G, s, E, par); break;
+    case 32: launch_slot_rows_t<16, false>(c, G, s, E, par); break;
+    case 33: launch_slot_rows_t<16, true>(c, G, s, E, par); break;
+    case 64: launch_slot_rows_t<32, false>(c, G, s, E, par); break;
+    default: launch_slot_rows_t<32, true>(c, G, s, E, par); break;
   }
   if (csc) {
     k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
@@ -1070,7 +1105,7 @@ static Engine make_engine(qpk_ctx* c) {
   for (int i = 0; i < 3; ++i) E.x[i] = c->x[i].p;
   E.r = c->r.p; E.p = c->p.p; E.y = c->y.p; E.zb = c->zb.p; E.minv = c->minv.p;
   E.part = c->part.p; E.G = c->grid_eng;
-  E.G_rows = (c->scatter == QPK_SCATTER_DICT) ? std::min(c->sms, c->grid_eng) : c->grid_eng;
+  E.G_rows = (c->scatter == QPK_SCATTER_DICT || use_tma_rows(c)) ? std::min(c->sms, c->grid_eng) : c->grid_eng;
   E.ctrl = c->ctrl.p; E.counter = c->counter.p; E.cfg = c->ecfg.p;
   E.seg_ptr = c->seg_ptr.p; E.seg_beg = c->seg_beg.p; E.seg_sum = c->seg_sum.p;
   E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
