@@ -99,6 +99,16 @@ int qpk_destroy(qpk_ctx* ctx);
 int qpk_set_stream(qpk_ctx* ctx, void* stream);
 int qpk_synchronize(qpk_ctx* ctx);
 
+/* ---- multi-GPU: row sharding of B over ranks (one process per GPU) ------
+ * Rank r holds rows [lo_r, hi_r) of B and the matching slice of every bottom
+ * vector; the top block (n) is replicated.  Per PCG iteration the ranks
+ * all-reduce [y_top partial | 4 scalars] and [r'r, r'z] with NCCL (SURVEY.md
+ * 8(e)).  Rank 0 obtains the id, the launcher broadcasts it (e.g. through
+ * torch.distributed), every rank calls qpk_shard_init before
+ * qpk_problem_begin with its local sizes. */
+int qpk_nccl_get_unique_id(unsigned char id[128]);
+int qpk_shard_init(qpk_ctx* ctx, int world, int rank, const unsigned char id[128]);
+
 /* ---- problem upload (once per QpProblem) ------------------------------ */
 /* n variables; m_e equality rows (C), m_l rows of A with a finite lower bound,
  * m_u rows of A with a finite upper bound; m_B = m_e + m_l + m_u. */

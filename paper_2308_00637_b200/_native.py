@@ -27,6 +27,7 @@ EXPORTED = (
     "qpk_set_hessian_csr", "qpk_set_hessian_dense", "qpk_set_hessian_lowrank",
     "qpk_problem_finalize", "qpk_set_diagonals", "qpk_set_diagonals_dev", "qpk_jacobi",
     "qpk_apply", "qpk_apply_dev", "qpk_pcg", "qpk_pcg_dev", "qpk_query",
+    "qpk_nccl_get_unique_id", "qpk_shard_init",
 )
 
 
@@ -77,6 +78,8 @@ _SIGS = {
     "qpk_pcg": ([_P, _P, _D, _I, _I64, _P, ctypes.POINTER(PcgInfo), _P], _I),
     "qpk_pcg_dev": ([_P, _P, _D, _I, _I64, _P, ctypes.POINTER(PcgInfo), _P], _I),
     "qpk_query": ([_P, ctypes.c_char_p], _I64),
+    "qpk_nccl_get_unique_id": ([_P], _I),
+    "qpk_shard_init": ([_P, _I, _I, _P], _I),
 }
 
 _lib = None

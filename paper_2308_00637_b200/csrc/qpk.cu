@@ -21,6 +21,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <dlfcn.h>
 
 #include "../../include/qpk.h"
 #include "qpk_device.cuh"
@@ -371,6 +372,8 @@ __global__ void k_hdiag(Hess H, int n, double* out) {
 }
 
 // ============================================================= host side ===
+struct QpkNcclId { char internal[128]; };
+
 namespace {
 
 thread_local std::string g_err;
@@ -417,6 +420,39 @@ int pow2_clamp(long long v, int lo, int hi) {
   while (p < v && p < hi) p <<= 1;
   return std::max(lo, std::min(hi, p));
 }
+
+// ---- NCCL, loaded at run time (the process's own libnccl.so.2: torch's when
+// torch is loaded, so only one NCCL is ever in the process) ----
+struct NcclApi {
+  bool tried = false, ok = false;
+  int (*getUniqueId)(void*) = nullptr;
+  int (*commInitRank)(void**, int, QpkNcclId, int) = nullptr;
+  int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*groupStart)() = nullptr;
+  int (*groupEnd)() = nullptr;
+  int (*commDestroy)(void*) = nullptr;
+  const char* (*errStr)(int) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  api.getUniqueId = (int (*)(void*))dlsym(h, "ncclGetUniqueId");
+  api.commInitRank = (int (*)(void**, int, QpkNcclId, int))dlsym(h, "ncclCommInitRank");
+  api.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(h, "ncclAllReduce");
+  api.groupStart = (int (*)())dlsym(h, "ncclGroupStart");
+  api.groupEnd = (int (*)())dlsym(h, "ncclGroupEnd");
+  api.commDestroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+  api.errStr = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+  api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.groupStart && api.groupEnd && api.commDestroy;
+  return api;
+}
+
+constexpr int NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
 }  // namespace
 
@@ -469,6 +505,12 @@ struct qpk_ctx {
   DBuf<PcgOut> out;
   int grid_pcg = 0, grid_std = 0;
 
+  // row sharding over ranks (one process per GPU)
+  int world = 1, rank = 0;
+  bool sharded = false;
+  void* comm = nullptr;
+  DBuf<double> gscal, lscal2, abuf;
+
   // slot engine
   int engine = -1;               // -1 auto, 0 persistent kernel, 1 slot engine
   int grid_eng = 0;
@@ -489,6 +531,7 @@ struct qpk_ctx {
     o.H.kind = hkind; o.H.h = hh.p; o.H.rp = hrp.p; o.H.ci = hci.p; o.H.v = hv.p; o.H.lanes = h_lanes;
     o.H.dense = hdense.p; o.H.U = U.p; o.H.w = w.p; o.H.k = (int)hk;
     o.d = d.p; o.q = q.p;
+    o.top_owner = rank == 0 ? 1 : 0;
     return o;
   }
   long long N() const { return n + m; }
@@ -576,6 +619,7 @@ int qpk_destroy(qpk_ctx* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
   for (auto& e : c->poll_ev) if (e) cudaEventDestroy(e);
   if (c->pinned_mode) cudaFreeHost(c->pinned_mode);
   if (c->own) cudaStreamDestroy(c->own);
@@ -593,6 +637,29 @@ int qpk_synchronize(qpk_ctx* c) {
   if (!c) return fail(QPK_E_ARG, "null context");
   CUDA_TRY(cudaSetDevice(c->device));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+int qpk_nccl_get_unique_id(unsigned char* id) {
+  if (!id) return fail(QPK_E_ARG, "qpk_nccl_get_unique_id: null buffer");
+  if (!nccl().ok) return fail(QPK_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+  const int rc = nccl().getUniqueId(id);
+  if (rc != 0) return fail(QPK_E_CUDA, "ncclGetUniqueId failed (%d)", rc);
+  return QPK_OK;
+}
+
+int qpk_shard_init(qpk_ctx* c, int world, int rank, const unsigned char* id) {
+  if (!c || world < 1 || rank < 0 || rank >= world || !id) return fail(QPK_E_ARG, "qpk_shard_init: bad arguments");
+  if (c->building || c->finalized) return fail(QPK_E_STATE, "qpk_shard_init must precede qpk_problem_begin");
+  if (!nccl().ok) return fail(QPK_E_UNSUPPORTED, "libnccl.so.2 not loadable");
+  CUDA_TRY(cudaSetDevice(c->device));
+  QpkNcclId uid;
+  memcpy(uid.internal, id, sizeof uid.internal);
+  const int rc = nccl().commInitRank(&c->comm, world, uid, rank);
+  if (rc != 0) return fail(QPK_E_CUDA, "ncclCommInitRank failed: %s", nccl().errStr ? nccl().errStr(rc) : "?");
+  c->world = world;
+  c->rank = rank;
+  c->sharded = true;
   return QPK_OK;
 }
 
@@ -964,6 +1031,14 @@ int qpk_set_diagonals_dev(qpk_ctx* c, const double* dd, const double* qq) {
   return set_diagonals(c, dd, qq, cudaMemcpyDeviceToDevice);
 }
 
+// in-place sum over ranks on the context's stream (sharded mode only)
+static int allreduce_sum(qpk_ctx* c, double* buf, size_t count, cudaStream_t s) {
+  if (!c->sharded || count == 0) return QPK_OK;
+  const int rc = nccl().allReduce(buf, buf, count, NCCL_FLOAT64, NCCL_SUM, c->comm, s);
+  if (rc != 0) return fail(QPK_E_CUDA, "ncclAllReduce failed: %s", nccl().errStr ? nccl().errStr(rc) : "?");
+  return QPK_OK;
+}
+
 static int build_jacobi(qpk_ctx* c) {
   Op o = c->op();
   const int G = c->grid_std;
@@ -973,7 +1048,15 @@ static int build_jacobi(qpk_ctx* c) {
     if (rc) return rc;
     Engine E = make_engine(c);
     k_jac_dict<<<c->grid_eng, QPK_DICT_WARPS * 32, DICT_SMEM, s>>>(E);
-    k_jac_dict_finish<<<G, QPK_BLOCK, 0, s>>>(E, c->hdiag.p, c->jac.p, c->minv.p);
+    if (c->sharded) {
+      // local column sums, summed over ranks, then the common finish
+      k_dict_col_sum<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p);
+      int rc2 = allreduce_sum(c, c->y.p, c->n, s);
+      if (rc2) return rc2;
+      k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
+    } else {
+      k_jac_dict_finish<<<G, QPK_BLOCK, 0, s>>>(E, c->hdiag.p, c->jac.p, c->minv.p);
+    }
     c->launches += 2;
     CUDA_TRY(cudaGetLastError());
     c->jac_ready = true;
@@ -984,6 +1067,10 @@ static int build_jacobi(qpk_ctx* c) {
     if (c->have_csc) k_jac_cols<<<G, QPK_BLOCK, 0, s>>>(o, c->y.p);
     else launch_jac_rows(c->lanes, G, s, o, c->y.p);
     c->launches++;
+  }
+  {
+    int rc2 = allreduce_sum(c, c->y.p, c->n, s);       // sharded: sum the ranks' B^2/D partials
+    if (rc2) return rc2;
   }
   k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
   c->launches++;
@@ -1015,7 +1102,7 @@ static int apply_impl(qpk_ctx* c, const double* v_dev, double* y_dev) {
   c->launches += 2;
   if (csc) { k_finish_csc<<<G, QPK_BLOCK, 0, s>>>(o, y_dev, c->zb.p); c->launches++; }
   CUDA_TRY(cudaGetLastError());
-  return QPK_OK;
+  return allreduce_sum(c, y_dev, c->n, s);          // sharded: y_top = sum of the ranks' partials
 }
 
 int qpk_apply(qpk_ctx* c, const double* v, double* y) {
@@ -1074,28 +1161,42 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
     T.blk_tile = c->blk_tile.p;
     T.tile_desc = c->tile_desc.p;
     k_slot_rows_tma<<<E.G_rows, (QPK_DICT_WARPS + 1) * 32, sizeof(TmaSmem), s>>>(E, T, par);
-    k_slot_update<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  } else {
+    switch (c->lanes * 2 + (csc ? 1 : 0)) {
+      case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
+      case 3: launch_slot_rows_t<1, true>(c, G, s, E, par); break;
+      case 4: launch_slot_rows_t<2, false>(c, G, s, E, par); break;
+      case 5: launch_slot_rows_t<2, true>(c, G, s, E, par); break;
+      case 8: launch_slot_rows_t<4, false>(c, G, s, E, par); break;
+      case 9: launch_slot_rows_t<4, true>(c, G, s, E, par); break;
+      case 16: launch_slot_rows_t<8, false>(c, G, s, E, par); break;
+      case 17: launch_slot_rows_t<8, true>(c, G, s, E, par); break;
+      case 32: launch_slot_rows_t<16, false>(c, G, s, E, par); break;
+      case 33: launch_slot_rows_t<16, true>(c, G, s, E, par); break;
+      case 64: launch_slot_rows_t<32, false>(c, G, s, E, par); break;
+      default: launch_slot_rows_t<32, true>(c, G, s, E, par); break;
+    }
+    if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
+  }
+  if (!c->sharded) {
+    if (c->scatter == QPK_SCATTER_DICT) k_slot_update<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
+    else if (csc) k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
+    else k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
     return;
   }
-  switch (c->lanes * 2 + (csc ? 1 : 0)) {
-    case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
-    case 3: launch_slot_rows_t<1, true>(c, G, s, E, par); break;
-    case 4: launch_slot_rows_t<2, false>(c, G, s, E, par); break;
-    case 5: launch_slot_rows_t<2, true>(c, G, s, E, par); break;
-    case 8: launch_slot_rows_t<4, false>(c, G, s, E, par); break;
-    case 9: launch_slot_rows_t<4, true>(c, G, s, E, par); break;
-    case 16: launch_slot_rows_t<8, false>(c, G, s, E, par); break;
-    case 17: launch_slot_rows_t<8, true>(c, G, s, E, par); break;
-    case 32: launch_slot_rows_t<16, false>(c, G, s, E, par); break;
-    case 33: launch_slot_rows_t<16, true>(c, G, s, E, par); break;
-    case 64: launch_slot_rows_t<32, false>(c, G, s, E, par); break;
-    default: launch_slot_rows_t<32, true>(c, G, s, E, par); break;
-  }
-  if (csc) {
-    k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
-    k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
-  }
-  else k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  // sharded: finish the local top block and scalars, one grouped all-reduce
+  // of [y_top | scalars], the update on the now-global y, an all-reduce of
+  // r'r and r'z, and the control decision.
+  if (c->scatter == QPK_SCATTER_DICT) k_shard_reduce<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  else if (csc) k_shard_reduce<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  else k_shard_reduce<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  nccl().groupStart();
+  allreduce_sum(c, c->y.p, c->n, s);
+  allreduce_sum(c, c->gscal.p, 4, s);
+  nccl().groupEnd();
+  k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  allreduce_sum(c, c->lscal2.p, 2, s);
+  k_slot_decide<<<1, 32, 0, s>>>(E, par);
 }
 
 static Engine make_engine(qpk_ctx* c) {
@@ -1110,6 +1211,8 @@ static Engine make_engine(qpk_ctx* c) {
   E.seg_ptr = c->seg_ptr.p; E.seg_beg = c->seg_beg.p; E.seg_sum = c->seg_sum.p;
   E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
   E.scatter = c->scatter;
+  E.sharded = c->sharded ? 1 : 0;
+  E.gscal = c->gscal.p; E.lscal2 = c->lscal2.p; E.abuf = c->abuf.p;
   E.dict.nblk = c->nblk; E.dict.blk_row = c->blk_row.p; E.dict.blk_dict = c->blk_dict.p; E.dict.cols = c->dcols.p;
   E.dict.lci = c->lci.p; E.dict.bpart = c->bpart.p; E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
   return E;
@@ -1121,6 +1224,9 @@ static int engine_setup(qpk_ctx* c) {
   CUDA_TRY(cudaFuncSetAttribute(k_jac_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
   CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TmaSmem)));
   CUDA_TRY(c->ctrl.alloc(2));
+  CUDA_TRY(c->gscal.alloc(4));
+  CUDA_TRY(c->lscal2.alloc(2));
+  CUDA_TRY(c->abuf.alloc(2));
   CUDA_TRY(c->counter.alloc(1));
   CUDA_TRY(c->ecfg.alloc(1));
   CUDA_TRY(cudaMemsetAsync(c->counter.p, 0, sizeof(unsigned int), c->stream));
@@ -1160,6 +1266,12 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
   Engine E = make_engine(c);
   k_engine_init<<<c->grid_eng, QPK_BLOCK, 0, s>>>(E);
   c->launches++;
+  if (c->sharded) {
+    rc = allreduce_sum(c, c->lscal2.p, 1, s);      // ||rhs||^2 over ranks
+    if (rc) return rc;
+    k_engine_init2<<<1, 32, 0, s>>>(E);
+    c->launches++;
+  }
   CUDA_TRY(cudaGetLastError());
   // upper bound on slots: every iteration may be followed by a check, + final
   const long long max_slots = 2 * max_iters + 4;
@@ -1171,7 +1283,7 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
     } else {
       for (int k = 0; k < CH; ++k) launch_slot(c, E, k & 1, s);
     }
-    c->launches += (c->scatter == QPK_SCATTER_CSC ? 4 : 3) * CH;
+    c->launches += (3 + (c->scatter == QPK_SCATTER_CSC ? 1 : 0) + (c->sharded ? 2 : 0)) * CH;
     slots += CH;
     const int b = chunk & 1;
     CUDA_TRY(cudaMemcpyAsync(&c->pinned_mode[b], &c->ctrl.p[0].mode, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1198,7 +1310,7 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
 extern "C" {
 
 static bool use_engine(qpk_ctx* c) {
-  if (c->scatter == QPK_SCATTER_DICT) return true;   // only the slot engine has the dictionary kernels
+  if (c->scatter == QPK_SCATTER_DICT || c->sharded) return true;   // dictionary kernels / collectives: engine only
   if (c->engine >= 0) return c->engine == 1;
   const char* env = getenv("QPK_ENGINE");
   if (env) return atoi(env) == 1;
@@ -1308,6 +1420,8 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "grid") return c->grid_pcg;
   if (k == "grid_engine") return c->grid_eng;
   if (k == "engine") return use_engine(c) ? 1 : 0;
+  if (k == "world") return c->world;
+  if (k == "rank") return c->rank;
   if (k == "dict_blocks") return c->nblk;
   if (k == "dict_reuse_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "block") return QPK_BLOCK;

@@ -40,6 +40,7 @@ struct Op {
   Hess H;
   const double* d;                      // d_diag, m
   const double* q;                      // q_diag_extra, n
+  int top_owner;                        // this rank adds the (replicated) top-block terms once
 };
 
 // partial-sum slots (slot-major: part[slot * G + cta])
@@ -101,6 +102,7 @@ __device__ __forceinline__ double subwarp_sum(double s) {
 // y_top = Q_diag-part * v (the part of Q u = H u + q_extra*u that is diagonal)
 // for element j, returns its contribution v_j * y_j to v'Kv.
 __device__ __forceinline__ double prep_elem(const Op& op, int j, double vj, double* y) {
+  if (!op.top_owner) { y[j] = 0.0; return 0.0; }     // other ranks: B'z partial only
   const int kind = op.H.kind;
   double qv = __dmul_rn(__ldg(op.q + j), vj);
   double t;
@@ -166,6 +168,7 @@ struct RowFuse {
 __device__ __forceinline__ double hess_rows(const Op& op, const double* u, double* y, const double* part, int G,
                                             double* red, double* s_lr) {
   double acc = 0.0;
+  if (!op.top_owner) return 0.0;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarp = (gridDim.x * blockDim.x) >> 5;
   const int kind = op.H.kind;

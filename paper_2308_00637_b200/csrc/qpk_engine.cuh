@@ -65,6 +65,10 @@ struct Engine {
   Op op;
   Dict dict;
   int scatter;                // 1 atomic, 2 CSC segments, 3 row-block dictionary
+  int sharded;                // row-sharded over ranks: collectives between the slot kernels
+  double* gscal;              // [4] rank-summed ROWS, PREP, AUX, AUX2 totals (sharded)
+  double* lscal2;             // [2] r'r, r'z (rank-local, then rank-summed)
+  double* abuf;               // [2] alpha and the r'z it used (identical on every rank)
   const int* seg_ptr;         // CSC segments: column j owns segments [seg_ptr[j], seg_ptr[j+1])
   const int* seg_beg;         // segment q covers padded CSC entries [seg_beg[q], seg_beg[q+1])
   double* seg_sum;            // per-segment partial of (B'z)
@@ -100,24 +104,10 @@ __device__ __forceinline__ bool last_block(unsigned int* counter) {
   return am_last;
 }
 
-// ----------------------------------------------------------------- init ----
-// x0 = 0, r = rhs (linalg.py:85-87); last block: ||rhs||, threshold
-// (linalg.py:83), early return when rnorm <= threshold (linalg.py:93-94).
-__global__ void __launch_bounds__(QPK_BLOCK) k_engine_init(Engine E) {
-  __shared__ double red[32];
-  const int N = E.op.n + E.op.m;
-  double acc = 0.0;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    const double b = __ldg(E.rhs + i);
-    E.x[0][i] = 0.0;
-    E.r[i] = b;
-    acc += b * b;
-  }
-  const double t = block_sum(acc, red);
-  if (threadIdx.x == 0) E.part[SLOT_AUX * E.G + blockIdx.x] = t;
-  if (!last_block(E.counter)) return;
-  const double rn = sqrt(grid_total(E.part + SLOT_AUX * E.G, E.G, red));
-  if (threadIdx.x == 0) {
+// initial control state from ||rhs||^2 (linalg.py:83, 93-94)
+__device__ __forceinline__ void engine_init_state(const Engine& E, double rr0) {
+  const double rn = sqrt(rr0);
+  {
     const EngineCfg cfg = *E.cfg;
     Ctrl c;
     memset(&c, 0, sizeof c);
@@ -132,6 +122,35 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_engine_init(Engine E) {
     if (cfg.hist) cfg.hist[0] = rn;
     E.ctrl[0] = c;
   }
+}
+
+// ----------------------------------------------------------------- init ----
+// x0 = 0, r = rhs (linalg.py:85-87); last block: ||rhs||, threshold
+// (linalg.py:83), early return when rnorm <= threshold (linalg.py:93-94).
+__global__ void __launch_bounds__(QPK_BLOCK) k_engine_init(Engine E) {
+  __shared__ double red[32];
+  const int N = E.op.n + E.op.m;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const double b = __ldg(E.rhs + i);
+    E.x[0][i] = 0.0;
+    E.r[i] = b;
+    if (E.op.top_owner || i >= E.op.n) acc += b * b;
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) E.part[SLOT_AUX * E.G + blockIdx.x] = t;
+  if (!last_block(E.counter)) return;
+  const double rr0 = grid_total(E.part + SLOT_AUX * E.G, E.G, red);
+  if (threadIdx.x == 0) {
+    E.ctrl[1].mode = MODE_NORMAL;        // never a stale DONE from a previous solve
+    if (E.sharded) { E.lscal2[0] = rr0; return; }   // summed over ranks, then k_engine_init2
+    engine_init_state(E, rr0);
+  }
+}
+
+// after the rank-sum of ||rhs||^2 (sharded)
+__global__ void k_engine_init2(Engine E) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) engine_init_state(E, E.lscal2[0]);
 }
 
 // ------------------------------------------------------------------ top ----
@@ -156,7 +175,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
       if (c.xupd) xd[j] = __dadd_rn(xs[j], __dmul_rn(c.alpha_prev, pold));
       const double rj = E.r[j];
       const double zj = __dmul_rn(__ldg(E.minv + j), rj);
-      rz += rj * zj;
+      if (op.top_owner) rz += rj * zj;
       const double pn = restart ? zj : __dadd_rn(zj, __dmul_rn(c.beta, pold));
       E.p[j] = pn;
       acc += prep_elem(op, j, pn, E.y);
@@ -409,90 +428,40 @@ __global__ void k_jac_dict_finish(Engine E, const double* hdiag, double* jac, do
   }
 }
 
-// --------------------------------------------------------------- update ----
+// Sharded slot: finish this rank's top block (y_top + its local B'z
+// partials) and the rank-local totals of the slot's scalar partials, both
+// then summed over ranks by one grouped all-reduce.
 template <int SC>
-__global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
-  constexpr bool CSC = SC != 1;
+__global__ void __launch_bounds__(QPK_BLOCK) k_shard_reduce(Engine E, int par) {
   __shared__ double red[32];
   const Ctrl c = E.ctrl[par];
-  if (c.mode == MODE_DONE) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par ^ 1] = c;
-    return;
-  }
-  const unsigned long long t_upd = globaltimer_ns();
-  const Op& op = E.op;
-  const int G = E.G;
-  const int N = op.n + op.m;
-  double rr = 0.0, rzn = 0.0;
-  double alpha = 0.0, rz = c.rz;
-  if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
-    const double pap = grid_total(E.part + SLOT_ROWS * G, E.G_rows, red) + grid_total(E.part + SLOT_PREP * G, G, red);
-    if (c.mode == MODE_RESTART)
-      rz = grid_total(E.part + SLOT_AUX * G, G, red) + grid_total(E.part + SLOT_AUX2 * G, E.G_rows, red);
-    if (pap <= 0.0) {                                                   // linalg.py:102-103
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
-        Ctrl o = c;
-        o.mode = MODE_DONE;
-        o.status = QPK_PCG_BREAKDOWN;
-        o.converged = 0;
-        o.applies += 1;
-        o.final_norm = c.best_rnorm;
-        o.result = c.best;
-        E.ctrl[par ^ 1] = o;
-      }
-      return;
-    }
-    alpha = rz / pap;
-    if (!CSC) {
-      const int np = N >> 1;
-      double2* r2 = reinterpret_cast<double2*>(E.r);
-      const double2* y2 = reinterpret_cast<const double2*>(E.y);
-      const double2* m2 = reinterpret_cast<const double2*>(E.minv);
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
-        double2 ri = r2[i];
-        const double2 yi = y2[i];
-        const double2 mi = __ldg(m2 + i);
-        ri.x = __dsub_rn(ri.x, __dmul_rn(alpha, yi.x));
-        ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yi.y));
-        r2[i] = ri;
-        rr += ri.x * ri.x + ri.y * ri.y;
-        rzn += ri.x * __dmul_rn(mi.x, ri.x) + ri.y * __dmul_rn(mi.y, ri.y);
-      }
-      if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
-        const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
-        E.r[N - 1] = ri;
-        rr += ri * ri;
-        rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
-      }
-    } else {
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-        const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
-        const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
-        E.r[i] = ri;
-        rr += ri * ri;
-        rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
-      }
-    }
-  } else {
-    // explicit residual rhs - K x (CHECK stores it as the new r; FINAL only needs its norm)
-    const bool store = c.mode == MODE_CHECK;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-      const double yi = (CSC && i < op.n) ? top_value<SC>(E, i) : E.y[i];
-      const double ri = __dsub_rn(__ldg(E.rhs + i), yi);
-      if (store) E.r[i] = ri;
-      rr += ri * ri;
-    }
-  }
-  double t = block_sum(rr, red);
-  if (threadIdx.x == 0) E.part[SLOT_RR * G + blockIdx.x] = t;
-  t = block_sum(rzn, red);
-  if (threadIdx.x == 0) E.part[SLOT_RZ * G + blockIdx.x] = t;
+  if (c.mode == MODE_DONE) return;
+  if (SC != 1)
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x)
+      E.y[j] = top_value<SC>(E, j);
   if (!last_block(E.counter)) return;
+  const int G = E.G;
+  const double t0 = grid_total(E.part + SLOT_ROWS * G, E.G_rows, red);
+  const double t1 = grid_total(E.part + SLOT_PREP * G, G, red);
+  const double t2 = grid_total(E.part + SLOT_AUX * G, G, red);
+  const double t3 = grid_total(E.part + SLOT_AUX2 * G, E.G_rows, red);
+  if (threadIdx.x == 0) { E.gscal[0] = t0; E.gscal[1] = t1; E.gscal[2] = t2; E.gscal[3] = t3; }
+}
 
-  // ---- decision (one block) ----
-  const double rr_tot = grid_total(E.part + SLOT_RR * G, G, red);
-  const double rz_tot = grid_total(E.part + SLOT_RZ * G, G, red);
-  if (threadIdx.x != 0) return;
+// column sums of the dictionary block partials (Jacobi in sharded mode)
+__global__ void k_dict_col_sum(Engine E, double* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
+    for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
+    out[j] = s;
+  }
+}
+
+// The PCG control decision after a slot (one thread): next mode, iteration
+// count, best iterate, beta -- linalg.py:104-133 for the scalars.
+__device__ __forceinline__ void decide(const Engine& E, const Ctrl& c, int par, double rr_tot, double rz_tot,
+                                       double alpha, double rz, unsigned long long t_upd) {
   const EngineCfg cfg = *E.cfg;
   const unsigned long long now = globaltimer_ns();
   Ctrl o = c;
@@ -545,6 +514,122 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
     o.xupd = 0;
   }
   E.ctrl[par ^ 1] = o;
+}
+
+// --------------------------------------------------------------- update ----
+template <int SC>
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
+  constexpr bool CSC = SC != 1;
+  __shared__ double red[32];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par ^ 1] = c;
+    return;
+  }
+  const unsigned long long t_upd = globaltimer_ns();
+  const Op& op = E.op;
+  const int G = E.G;
+  const int N = op.n + op.m;
+  double rr = 0.0, rzn = 0.0;
+  double alpha = 0.0, rz = c.rz;
+  if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
+    double pap;
+    if (E.sharded) {
+      pap = E.gscal[0] + E.gscal[1];
+      if (c.mode == MODE_RESTART) rz = E.gscal[2] + E.gscal[3];
+    } else {
+      pap = grid_total(E.part + SLOT_ROWS * G, E.G_rows, red) + grid_total(E.part + SLOT_PREP * G, G, red);
+      if (c.mode == MODE_RESTART)
+        rz = grid_total(E.part + SLOT_AUX * G, G, red) + grid_total(E.part + SLOT_AUX2 * G, E.G_rows, red);
+    }
+    if (pap <= 0.0) {                                                   // linalg.py:102-103
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Ctrl o = c;
+        o.mode = MODE_DONE;
+        o.status = QPK_PCG_BREAKDOWN;
+        o.converged = 0;
+        o.applies += 1;
+        o.final_norm = c.best_rnorm;
+        o.result = c.best;
+        E.ctrl[par ^ 1] = o;
+      }
+      return;
+    }
+    alpha = rz / pap;
+    if (!CSC) {
+      const int np = N >> 1;
+      double2* r2 = reinterpret_cast<double2*>(E.r);
+      const double2* y2 = reinterpret_cast<const double2*>(E.y);
+      const double2* m2 = reinterpret_cast<const double2*>(E.minv);
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
+        double2 ri = r2[i];
+        const double2 yi = y2[i];
+        const double2 mi = __ldg(m2 + i);
+        ri.x = __dsub_rn(ri.x, __dmul_rn(alpha, yi.x));
+        ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yi.y));
+        r2[i] = ri;
+        // replicated top entries count once over the ranks (rank 0)
+        const bool cx = op.top_owner || 2 * i >= op.n, cy = op.top_owner || 2 * i + 1 >= op.n;
+        if (cx) { rr += ri.x * ri.x; rzn += ri.x * __dmul_rn(mi.x, ri.x); }
+        if (cy) { rr += ri.y * ri.y; rzn += ri.y * __dmul_rn(mi.y, ri.y); }
+      }
+      if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+        const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
+        E.r[N - 1] = ri;
+        if (op.top_owner || N - 1 >= op.n) {
+          rr += ri * ri;
+          rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
+        }
+      }
+    } else {
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+        const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
+        const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
+        E.r[i] = ri;
+        if (op.top_owner || i >= op.n) {
+          rr += ri * ri;
+          rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
+        }
+      }
+    }
+  } else {
+    // explicit residual rhs - K x (CHECK stores it as the new r; FINAL only needs its norm)
+    const bool store = c.mode == MODE_CHECK;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+      const double yi = (CSC && i < op.n) ? top_value<SC>(E, i) : E.y[i];
+      const double ri = __dsub_rn(__ldg(E.rhs + i), yi);
+      if (store) E.r[i] = ri;
+      if (op.top_owner || i >= op.n) rr += ri * ri;
+    }
+  }
+  double t = block_sum(rr, red);
+  if (threadIdx.x == 0) E.part[SLOT_RR * G + blockIdx.x] = t;
+  t = block_sum(rzn, red);
+  if (threadIdx.x == 0) E.part[SLOT_RZ * G + blockIdx.x] = t;
+  if (!last_block(E.counter)) return;
+
+  // ---- decision (one block) ----
+  const double rr_tot = grid_total(E.part + SLOT_RR * G, G, red);
+  const double rz_tot = grid_total(E.part + SLOT_RZ * G, G, red);
+  if (threadIdx.x != 0) return;
+  if (E.sharded) {
+    // rank-local totals; summed over ranks by the collective, then k_slot_decide
+    E.lscal2[0] = rr_tot;
+    E.lscal2[1] = rz_tot;
+    E.abuf[0] = alpha;
+    E.abuf[1] = rz;
+    E.ctrl[par].t_upd = t_upd;
+    return;
+  }
+  decide(E, c, par, rr_tot, rz_tot, alpha, rz, t_upd);
+}
+
+// decision after a sharded slot: the collective has summed rr / rz over ranks
+__global__ void k_slot_decide(Engine E, int par) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE || E.ctrl[par ^ 1].mode == MODE_DONE) return;   // done, or breakdown already decided
+  decide(E, c, par, E.lscal2[0], E.lscal2[1], E.abuf[0], E.abuf[1], c.t_upd);
 }
 
 }  // namespace qpk
