@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--iters", type=int, default=500, help="PCG iterations per step (BASELINE cfg5: 500)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink cfg5 (testing only; 1.0 = BASELINE)")
-    ap.add_argument("--scatter", type=int, default=1, help="1 = atomic B'z, 2 = CSC gather (deterministic)")
+    ap.add_argument("--scatter", type=int, default=0,
+                    help="0 = auto per matrix, 1 = atomic B'z, 2 = CSC gather, 3 = row-block dictionary")
     ap.add_argument("--cpu-iters", type=int, default=10, help="oracle iterations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters-per-step", type=int, default=5)
@@ -227,17 +228,27 @@ def run_ours(args):
     from paper_2308_00637_b200.direction import GpuKkt, gpu_direction, operator_for
     from paper_2308_00637_b200.pcg import PcgConfig
 
-    problem, op, rhs, meta = make_workload(args.workload, args.scale, seed_offset=rank)
-    gk = GpuKkt(problem, op.bmap, device=local, scatter=args.scatter)
+    sharded_run = world > 1
+    # N > 1: every rank builds the same system and owns a row shard of it
+    # (strong scaling); N = 1: the whole system on one GPU
+    problem, op, rhs, meta = make_workload(args.workload, args.scale, seed_offset=0)
+    if sharded_run:
+        from paper_2308_00637_b200.sharded import ShardedKkt
+        gk = ShardedKkt(problem, op.bmap, device=local, scatter=args.scatter)
+        rhs_loc = gk.local(rhs)
+        d_loc = np.ascontiguousarray(op.d_diag[gk.lo:gk.hi])
+    else:
+        gk = GpuKkt(problem, op.bmap, device=local, scatter=args.scatter)
+        rhs_loc, d_loc = rhs, np.ascontiguousarray(op.d_diag)
     stream = torch.cuda.current_stream()
     gk.ctx.call("qpk_set_stream", _native.ctypes.c_void_p(stream.cuda_stream))
     gk.set_diagonals(op.d_diag, op.q_diag_extra)
     gk.jacobi()
     N = op.dim
-    rhs_d = torch.from_numpy(rhs).to(f"cuda:{local}")
-    d_d = torch.from_numpy(np.ascontiguousarray(op.d_diag)).to(f"cuda:{local}")
+    rhs_d = torch.from_numpy(rhs_loc).to(f"cuda:{local}")
+    d_d = torch.from_numpy(d_loc).to(f"cuda:{local}")
     q_d = torch.from_numpy(np.ascontiguousarray(op.q_diag_extra)).to(f"cuda:{local}")
-    x_d = torch.empty(N, dtype=torch.float64, device=f"cuda:{local}")
+    x_d = torch.empty(len(rhs_loc), dtype=torch.float64, device=f"cuda:{local}")
     info = _native.PcgInfo()
 
     def step():
@@ -255,6 +266,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         step()
     assert info.iterations == args.iters and info.applies == args.iters + 1, (info.iterations, info.applies)
+    engine_used = gk.ctx.query("engine")
     barrier()
     launches0 = gk.ctx.query("kernel_launches")
     kernel_ms, phase_ms = [], []
@@ -273,18 +285,24 @@ def run_ours(args):
         t = torch.tensor([elapsed], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         elapsed = float(t.item())
-    total_iters = args.iters * args.steps * world
+    # one system solved jointly by all ranks when sharded (strong scaling)
+    total_iters = args.iters * args.steps
     value = total_iters / elapsed
 
     # e2e through the reference-facing drop-in, host buffers
     e2e_cfg = PcgConfig(tol=1e-300, max_iters=args.iters)
-    gk_cached = operator_for(op, device=local)       # one upload per problem (not timed)
-    gpu_direction(op, rhs, e2e_cfg)
+    if sharded_run:
+        from paper_2308_00637_b200.sharded import sharded_direction
+        direction = lambda o, b, c: sharded_direction(o, b, c, device=local)  # noqa: E731
+    else:
+        operator_for(op, device=local)               # one upload per problem (not timed)
+        direction = gpu_direction
+    direction(op, rhs, e2e_cfg)
     barrier()
     t0 = time.perf_counter()
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(e2e_steps):
-        res = gpu_direction(op, rhs, e2e_cfg)
+        res = direction(op, rhs, e2e_cfg)
         _ = float(res.final_residual_norm)
     barrier()
     e2e_dt = time.perf_counter() - t0
@@ -292,14 +310,14 @@ def run_ours(args):
         t = torch.tensor([e2e_dt], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_dt = float(t.item())
-    e2e_value = args.iters * e2e_steps * world / e2e_dt
-    h2d = 8 * (op.m + op.n + N)
-    d2h = 8 * N
+    e2e_value = args.iters * e2e_steps / e2e_dt
+    h2d = 8 * (len(d_loc) + op.n + len(rhs_loc))     # per rank: its diagonals + rhs slice
+    d2h = 8 * len(rhs_loc)
 
     # roofline of the dominant kernel (the persistent PCG kernel: one launch per step)
     per_launch, per_iter = algorithmic_bytes(op, args.iters, applies=1)
     avg_ms = float(np.mean(kernel_ms))
-    achieved = per_launch / (avg_ms * 1e-3) / 1e9
+    achieved = per_launch / world / (avg_ms * 1e-3) / 1e9     # per GPU
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
     traffic = None
@@ -314,21 +332,25 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator of BASELINE.json configs[4]; no dataset involved)",
             "config": {"workload": WORKLOAD_DESC[args.workload] + (f" (scale {args.scale})" if args.scale != 1 else "")
                                    + f"; {args.iters} PCG iterations per step (+ Jacobi build + final apply)",
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "scatter": "atomic" if args.scatter == 1 else "csc",
+                       "parallelism": f"rowshard{world} (NCCL all-reduce per iteration)" if world > 1 else "single",
+                       "scatter": {1: "atomic", 2: "csc", 3: "dict"}.get(gk.ctx.query("scatter"), "?"),
                        "l2": "inputs larger than L2" if per_iter > 126e6 else
                        "working set fits L2 (each step re-reads it every PCG iteration; no flush)",
                        "n": op.n, "m_B": op.m, "nnz_B": gk.ctx.query("nnz"),
                        "grid": gk.ctx.query("grid"), "lanes_per_row": gk.ctx.query("lanes"),
+                       "engine": "slot engine (per-phase kernels, CUDA graph)" if engine_used else
+                                 "persistent cooperative kernel",
                        "seed": meta["seed"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "algorithmic_bytes_per_launch": per_launch, "algorithmic_bytes_per_iter": per_iter,
-                         "kernel": f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if args.scatter == 2 else 'false'}>", "kernel_ms_avg": avg_ms,
+                         "kernel": ("slot engine kernels k_slot_top/rows/update (whole solve)" if engine_used else
+                                    f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if gk.ctx.query('scatter') == 2 else 'false'}>"),
+                         "kernel_ms_avg": avg_ms,
                          "phase_us_per_iter": dict(zip(["direction_top", "rows_B_Bt", "residual_update", "other"],
                                                        [round(v * 1e3 / args.iters, 2) for v in np.mean(phase_ms, axis=0)])),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
