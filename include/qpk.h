@@ -147,6 +147,40 @@ int qpk_pcg(qpk_ctx* ctx, const double* rhs, double tol, int tol_is_relative, in
 int qpk_pcg_dev(qpk_ctx* ctx, const double* rhs, double tol, int tol_is_relative, int64_t max_iters,
                 double* x, qpk_pcg_info* info, double* resid_hist_dev);
 
+/* ---- device-resident interior-point loop -------
+ * qpk_ipm_solve runs qpipm.ipm.solve (ipm.py:185-240) with the iterate,
+ * residuals, right-hand side, direction recovery, ratio test and step on the
+ * device; only the per-iteration scalars cross to the host.  Single GPU. */
+typedef struct {
+  double gamma, mu_init, mu_tol, mu_shrink;   /* IpmConfig (ipm.py:31-46) */
+  int64_t max_iters;
+  double pcg_tol;                             /* PcgConfig (linalg.py:29-39) */
+  int64_t pcg_max_iters;
+  int32_t pcg_tol_is_relative;
+  int32_t verbose;
+} qpk_ipm_config;
+
+typedef struct {                              /* TraceRecord (ipm.py:49-59) */
+  int32_t iter, cg_iters;
+  double mu, primal_inf, dual_inf, compl_inf, cg_resid, alpha_x, alpha_lam;
+} qpk_ipm_trace;
+
+typedef struct {
+  int32_t status;                             /* 0 converged, 1 iteration_limit, 2 linear_solver_failure */
+  int32_t iterations;
+  int64_t cg_total;
+  double objective;                           /* 1/2 x'Hx + p'x (model.py:257-258) */
+  double wall_ms;
+} qpk_ipm_result;
+
+/* p (n); bnd (m_B, B-row order: b of the C rows | lower bounds of the A_l rows
+ * | upper bounds of the A_u rows); variable bounds as index lists + values. */
+int qpk_ipm_set_bounds(qpk_ctx* ctx, const double* p, const double* bnd, int64_t n_lower, const int64_t* var_lower,
+                       const double* lower, int64_t n_upper, const int64_t* var_upper, const double* upper);
+/* x_out (n, nullable); trace (capacity cfg->max_iters records, nullable) */
+int qpk_ipm_solve(qpk_ctx* ctx, const qpk_ipm_config* cfg, double* x_out, qpk_ipm_trace* trace,
+                  qpk_ipm_result* result);
+
 /* ---- introspection ------------------------------------------------------ */
 /* keys: "n", "m", "nnz", "nnz_padded", "lanes", "scatter", "grid", "block",
  * "sms", "hess_kind", "device_bytes", "kernel_launches" */

@@ -27,7 +27,7 @@ EXPORTED = (
     "qpk_set_hessian_csr", "qpk_set_hessian_dense", "qpk_set_hessian_lowrank",
     "qpk_problem_finalize", "qpk_set_diagonals", "qpk_set_diagonals_dev", "qpk_jacobi",
     "qpk_apply", "qpk_apply_dev", "qpk_pcg", "qpk_pcg_dev", "qpk_query",
-    "qpk_nccl_get_unique_id", "qpk_shard_init",
+    "qpk_nccl_get_unique_id", "qpk_shard_init", "qpk_ipm_set_bounds", "qpk_ipm_solve",
 )
 
 
@@ -50,6 +50,24 @@ class PcgInfo(ctypes.Structure):
         ("rhs_norm", ctypes.c_double), ("kernel_ms", ctypes.c_double),
         ("phase_ms", ctypes.c_double * 4),
     ]
+
+
+class IpmConfig(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("mu_init", ctypes.c_double), ("mu_tol", ctypes.c_double),
+                ("mu_shrink", ctypes.c_double), ("max_iters", ctypes.c_int64), ("pcg_tol", ctypes.c_double),
+                ("pcg_max_iters", ctypes.c_int64), ("pcg_tol_is_relative", ctypes.c_int32),
+                ("verbose", ctypes.c_int32)]
+
+
+class IpmTrace(ctypes.Structure):
+    _fields_ = [("iter", ctypes.c_int32), ("cg_iters", ctypes.c_int32), ("mu", ctypes.c_double),
+                ("primal_inf", ctypes.c_double), ("dual_inf", ctypes.c_double), ("compl_inf", ctypes.c_double),
+                ("cg_resid", ctypes.c_double), ("alpha_x", ctypes.c_double), ("alpha_lam", ctypes.c_double)]
+
+
+class IpmResult(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int32), ("iterations", ctypes.c_int32), ("cg_total", ctypes.c_int64),
+                ("objective", ctypes.c_double), ("wall_ms", ctypes.c_double)]
 
 
 _P = ctypes.c_void_p
@@ -80,6 +98,8 @@ _SIGS = {
     "qpk_query": ([_P, ctypes.c_char_p], _I64),
     "qpk_nccl_get_unique_id": ([_P], _I),
     "qpk_shard_init": ([_P, _I, _I, _P], _I),
+    "qpk_ipm_set_bounds": ([_P, _P, _P, _I64, _P, _P, _I64, _P, _P], _I),
+    "qpk_ipm_solve": ([_P, ctypes.POINTER(IpmConfig), _P, _P, ctypes.POINTER(IpmResult)], _I),
 }
 
 _lib = None

@@ -27,6 +27,8 @@
 #include "qpk_device.cuh"
 #include "qpk_engine.cuh"
 #include "qpk_tma.cuh"
+#include "qpk_ipm.cuh"
+#include <chrono>
 
 namespace cg = cooperative_groups;
 using namespace qpk;
@@ -280,6 +282,13 @@ __global__ void __launch_bounds__(QPK_BLOCK, QPK_PCG_MIN_BLOCKS) pcg_kernel(PcgP
 }
 
 // ---------------------------------------------------- standalone phases ---
+// y += H' u for the non-diagonal Hessian kinds (after k_prep with q = 0)
+__global__ void __launch_bounds__(QPK_BLOCK) k_hess(Op op, const double* u, double* y, double* part, int G) {
+  __shared__ double red[32];
+  __shared__ double s_lr[QPK_KMAX];
+  hess_rows(op, u, y, part, G, red, s_lr);
+}
+
 __global__ void __launch_bounds__(QPK_BLOCK) k_prep(Op op, const double* v, double* y, double* part, int G) {
   __shared__ double red[32];
   phase_prep(op, v, y, part, G, red);
@@ -504,6 +513,17 @@ struct qpk_ctx {
   DBuf<double> x[3], r, p, y, zb, rhs, part, hist, vin;
   DBuf<PcgOut> out;
   int grid_pcg = 0, grid_std = 0;
+
+  // device-resident IPM (qpk_ipm_*)
+  bool ipm_ready = false;
+  long long nl = 0, nu = 0;
+  DBuf<int> vlo, vhi;
+  DBuf<double> ipm_lx, ipm_ux, ipm_bnd, ipm_p, ipm_x, ipm_sB, ipm_lamB, ipm_slx, ipm_sux, ipm_llx, ipm_lux;
+  DBuf<double> ipm_rH, ipm_rB, ipm_rcB, ipm_rlx, ipm_rux, ipm_rc3, ipm_rc4;
+  DBuf<double> ipm_dsB, ipm_dlamB, ipm_dslx, ipm_dsux, ipm_dllx, ipm_dlux;
+  DBuf<double> ipm_hx, ipm_t, ipm_btl, ipm_part, ipm_rhs, ipm_sol, ipm_w2, ipm_tmp, ipm_zero;
+  DBuf<double> ipm_lofull, ipm_hifull;
+  DBuf<unsigned char> ipm_haslo, ipm_hashi;
 
   // row sharding over ranks (one process per GPU)
   int world = 1, rank = 0;
@@ -1404,6 +1424,236 @@ int qpk_pcg(qpk_ctx* c, const double* rhs, double tol, int rel, int64_t max_iter
                              cudaMemcpyDeviceToHost, c->stream));
   }
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+// ------------------------------------------------------------ device IPM ---
+int qpk_ipm_set_bounds(qpk_ctx* c, const double* p, const double* bnd, int64_t nl, const int64_t* vlo,
+                       const double* lx, int64_t nu, const int64_t* vhi, const double* ux) {
+  if (!c || !c->finalized) return fail(QPK_E_STATE, "qpk_ipm_set_bounds: problem not finalized");
+  if (c->sharded) return fail(QPK_E_UNSUPPORTED, "device IPM is single-GPU");
+  if (!p || (c->m && !bnd) || nl < 0 || nu < 0 || nl > c->n || nu > c->n)
+    return fail(QPK_E_ARG, "qpk_ipm_set_bounds: bad arguments");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  const long long n = c->n, m = c->m, N = c->N();
+  std::vector<int> lo(nl), hi(nu);
+  std::vector<unsigned char> haslo(n, 0), hashi(n, 0);
+  std::vector<double> lof(n, 0.0), hif(n, 0.0);
+  for (long long k = 0; k < nl; ++k) {
+    if (vlo[k] < 0 || vlo[k] >= n) return fail(QPK_E_ARG, "variable bound index out of range");
+    lo[k] = (int)vlo[k]; haslo[vlo[k]] = 1; lof[vlo[k]] = lx[k];
+  }
+  for (long long k = 0; k < nu; ++k) {
+    if (vhi[k] < 0 || vhi[k] >= n) return fail(QPK_E_ARG, "variable bound index out of range");
+    hi[k] = (int)vhi[k]; hashi[vhi[k]] = 1; hif[vhi[k]] = ux[k];
+  }
+  c->nl = nl; c->nu = nu;
+  CUDA_TRY(upload(c->vlo, lo, s));
+  CUDA_TRY(upload(c->vhi, hi, s));
+  CUDA_TRY(upload(c->ipm_haslo, haslo, s));
+  CUDA_TRY(upload(c->ipm_hashi, hashi, s));
+  CUDA_TRY(upload(c->ipm_lofull, lof, s));
+  CUDA_TRY(upload(c->ipm_hifull, hif, s));
+  const std::vector<double> vlx(lx, lx + nl), vux(ux, ux + nu), vbnd(bnd, bnd + m), vp(p, p + n);
+  CUDA_TRY(upload(c->ipm_lx, vlx, s));
+  CUDA_TRY(upload(c->ipm_ux, vux, s));
+  CUDA_TRY(upload(c->ipm_bnd, vbnd, s));
+  CUDA_TRY(upload(c->ipm_p, vp, s));
+  for (DBuf<double>* b : {&c->ipm_x, &c->ipm_rH, &c->ipm_hx, &c->ipm_btl, &c->ipm_tmp, &c->ipm_zero})
+    CUDA_TRY(b->alloc(n + 8));
+  for (DBuf<double>* b : {&c->ipm_sB, &c->ipm_lamB, &c->ipm_rB, &c->ipm_rcB, &c->ipm_dsB, &c->ipm_dlamB,
+                          &c->ipm_t, &c->ipm_w2})
+    CUDA_TRY(b->alloc(m + 8));
+  for (DBuf<double>* b : {&c->ipm_slx, &c->ipm_llx, &c->ipm_rlx, &c->ipm_rc3, &c->ipm_dslx, &c->ipm_dllx})
+    CUDA_TRY(b->alloc(nl + 8));
+  for (DBuf<double>* b : {&c->ipm_sux, &c->ipm_lux, &c->ipm_rux, &c->ipm_rc4, &c->ipm_dsux, &c->ipm_dlux})
+    CUDA_TRY(b->alloc(nu + 8));
+  CUDA_TRY(c->ipm_rhs.alloc(N + 8));
+  CUDA_TRY(c->ipm_sol.alloc(N + 8));
+  CUDA_TRY(c->ipm_part.alloc(8 * (size_t)c->grid_std));
+  CUDA_TRY(cudaMemsetAsync(c->ipm_zero.p, 0, (n + 8) * sizeof(double), s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  c->ipm_ready = true;
+  return QPK_OK;
+}
+
+static IpmDev ipm_dev(qpk_ctx* c) {
+  IpmDev P;
+  P.n = (int)c->n; P.m = (int)c->m; P.me = (int)c->m_e; P.ml = (int)c->m_l; P.mu_rows = (int)c->m_u;
+  P.nl = (int)c->nl; P.nu = (int)c->nu;
+  P.vlo = c->vlo.p; P.vhi = c->vhi.p; P.lx = c->ipm_lx.p; P.ux = c->ipm_ux.p; P.bnd = c->ipm_bnd.p; P.pvec = c->ipm_p.p;
+  P.x = c->ipm_x.p; P.sB = c->ipm_sB.p; P.lamB = c->ipm_lamB.p;
+  P.slx = c->ipm_slx.p; P.sux = c->ipm_sux.p; P.llx = c->ipm_llx.p; P.lux = c->ipm_lux.p;
+  P.rH = c->ipm_rH.p; P.rB = c->ipm_rB.p; P.rcB = c->ipm_rcB.p; P.rlx = c->ipm_rlx.p; P.rux = c->ipm_rux.p;
+  P.rc3 = c->ipm_rc3.p; P.rc4 = c->ipm_rc4.p;
+  P.dsB = c->ipm_dsB.p; P.dlamB = c->ipm_dlamB.p; P.dslx = c->ipm_dslx.p; P.dsux = c->ipm_dsux.p;
+  P.dllx = c->ipm_dllx.p; P.dlux = c->ipm_dlux.p;
+  P.hx = c->ipm_hx.p; P.t = c->ipm_t.p; P.btl = c->ipm_btl.p; P.part = c->ipm_part.p; P.G = c->grid_std;
+  return P;
+}
+
+// H x into ipm_hx (prep with q = 0 gives the diagonal part, k_hess the rest)
+static void ipm_hess_apply(qpk_ctx* c, const double* xv, double* out) {
+  Op o = c->op();
+  o.q = c->ipm_zero.p;
+  o.top_owner = 1;
+  const int G = c->grid_std;
+  k_prep<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out, c->part.p, G);
+  k_hess<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out, c->part.p, G);
+  c->launches += 2;
+}
+
+static void ipm_bt(qpk_ctx* c, const double* w, double* out) {
+  const int G = c->grid_std;
+  cudaMemsetAsync(out, 0, c->n * sizeof(double), c->stream);
+  if (c->m) k_spmv_bt<<<G, QPK_BLOCK, 0, c->stream>>>(c->op(), w, out);
+  c->launches++;
+}
+
+// partial sums (sum or min) of `slots` slots, on the host
+static int ipm_read(qpk_ctx* c, int slots, std::vector<double>& h) {
+  const int G = c->grid_std;
+  h.resize((size_t)slots * G);
+  CUDA_TRY(cudaMemcpyAsync(h.data(), c->ipm_part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+static double slot_sum(const std::vector<double>& h, int slot, int G) {
+  double s = 0.0;
+  for (int i = 0; i < G; ++i) s += h[(size_t)slot * G + i];
+  return s;
+}
+static double slot_min(const std::vector<double>& h, int slot, int G) {
+  double s = INFINITY;
+  for (int i = 0; i < G; ++i) s = std::min(s, h[(size_t)slot * G + i]);
+  return s;
+}
+
+// residuals at the current iterate; returns (primal, dual, compl, full) norms
+static int ipm_residuals(qpk_ctx* c, double mu, double out[4], bool* finite) {
+  IpmDev P = ipm_dev(c);
+  const int G = c->grid_std;
+  cudaStream_t s = c->stream;
+  ipm_hess_apply(c, P.x, P.hx);
+  if (c->m) k_spmv_b<<<G, QPK_BLOCK, 0, s>>>(c->op(), P.x, P.t);
+  ipm_bt(c, P.lamB, P.btl);
+  k_ipm_residuals<<<G, QPK_BLOCK, 0, s>>>(P, mu);
+  k_ipm_rh_lo<<<G, QPK_BLOCK, 0, s>>>(P);
+  k_ipm_rh_hi<<<G, QPK_BLOCK, 0, s>>>(P);
+  k_ipm_dual_norm<<<G, QPK_BLOCK, 0, s>>>(P);
+  c->launches += 5;
+  CUDA_TRY(cudaGetLastError());
+  std::vector<double> h;
+  int rc = ipm_read(c, 6, h);
+  if (rc) return rc;
+  const double pr = slot_sum(h, 0, G), du = slot_sum(h, 1, G), co = slot_sum(h, 2, G), re = slot_sum(h, 3, G);
+  out[0] = sqrt(pr); out[1] = sqrt(du); out[2] = sqrt(co); out[3] = sqrt(pr + du + co + re);
+  *finite = slot_sum(h, 4, G) == 0.0 && slot_sum(h, 5, G) == 0.0;
+  return QPK_OK;
+}
+
+int qpk_ipm_solve(qpk_ctx* c, const qpk_ipm_config* cfg, double* x_out, qpk_ipm_trace* trace,
+                  qpk_ipm_result* res) {
+  if (!c || !c->ipm_ready) return fail(QPK_E_STATE, "qpk_ipm_solve: call qpk_ipm_set_bounds first");
+  if (!cfg || !res) return fail(QPK_E_ARG, "qpk_ipm_solve: null config/result");
+  if (!(cfg->gamma > 0.0 && cfg->gamma < 1.0)) return fail(QPK_E_ARG, "gamma must lie in (0, 1)");
+  if (cfg->mu_init <= 0 || cfg->mu_tol <= 0 || cfg->mu_shrink <= 1.0) return fail(QPK_E_ARG, "bad barrier parameters");
+  CUDA_TRY(cudaSetDevice(c->device));
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaStream_t s = c->stream;
+  IpmDev P = ipm_dev(c);
+  const int G = c->grid_std;
+  const long long n = c->n, m = c->m;
+  // initialize (ipm.py:73-104)
+  k_ipm_init_x_bounds<<<G, QPK_BLOCK, 0, s>>>(P, c->ipm_haslo.p, c->ipm_hashi.p, c->ipm_lofull.p, c->ipm_hifull.p);
+  if (m) k_spmv_b<<<G, QPK_BLOCK, 0, s>>>(c->op(), P.x, P.t);
+  k_ipm_init_state<<<G, QPK_BLOCK, 0, s>>>(P, cfg->mu_init);
+  c->launches += 3;
+  double mu = cfg->mu_init;
+  double nrm[4];
+  bool finite = true;
+  int rc = ipm_residuals(c, mu, nrm, &finite);
+  if (rc) return rc;
+  if (!finite) return fail(QPK_E_STATE, "non-finite residual encountered");
+  res->status = 1;                      // iteration_limit
+  res->iterations = 0;
+  res->cg_total = 0;
+  for (long long it = 1; it <= cfg->max_iters; ++it) {
+    // operator diagonals (kkt.py:190-202)
+    k_ipm_diagonals<<<G, QPK_BLOCK, 0, s>>>(P, mu, c->d.p, c->q.p);
+    k_ipm_qextra_lo<<<G, QPK_BLOCK, 0, s>>>(P, c->q.p);
+    k_ipm_qextra_hi<<<G, QPK_BLOCK, 0, s>>>(P, c->q.p);
+    c->diag_set = true;
+    c->jac_ready = false;
+    // right-hand side (kkt.py:242-257)
+    k_ipm_rhs<<<G, QPK_BLOCK, 0, s>>>(P, c->d.p, c->ipm_rhs.p, c->ipm_w2.p);
+    k_ipm_rhs_lo<<<G, QPK_BLOCK, 0, s>>>(P, c->ipm_rhs.p);
+    k_ipm_rhs_hi<<<G, QPK_BLOCK, 0, s>>>(P, c->ipm_rhs.p);
+    ipm_bt(c, c->ipm_w2.p, c->ipm_tmp.p);
+    k_ipm_rhs_top<<<G, QPK_BLOCK, 0, s>>>(P, c->ipm_rhs.p, c->ipm_tmp.p, c->ipm_part.p);
+    c->launches += 7;
+    CUDA_TRY(cudaGetLastError());
+    {
+      std::vector<double> h;
+      rc = ipm_read(c, 1, h);
+      if (rc) return rc;
+      if (slot_sum(h, 0, G) != 0.0) return fail(QPK_E_STATE, "non-finite right-hand side");
+    }
+    // direction (ipm.py:205-212): a breakdown returns the best iterate, as the
+    // reference's except-branch does
+    qpk_pcg_info info;
+    rc = pcg_impl(c, c->ipm_rhs.p, cfg->pcg_tol, cfg->pcg_tol_is_relative, cfg->pcg_max_iters, c->ipm_sol.p,
+                  &info, nullptr);
+    if (rc) return rc;
+    res->cg_total += info.iterations;
+    k_ipm_recover<<<G, QPK_BLOCK, 0, s>>>(P, c->ipm_sol.p);
+    c->launches++;
+    std::vector<double> h;
+    rc = ipm_read(c, 3, h);
+    if (rc) return rc;
+    if (slot_sum(h, 2, G) != 0.0) { res->status = 2; break; }   // LINEAR_SOLVER_FAILURE
+    const double ax = std::min(1.0, cfg->gamma * slot_min(h, 0, G));
+    const double al = std::min(1.0, cfg->gamma * slot_min(h, 1, G));
+    k_ipm_step<<<G, QPK_BLOCK, 0, s>>>(P, c->ipm_sol.p, ax, al);
+    c->launches++;
+    rc = ipm_read(c, 1, h);
+    if (rc) return rc;
+    if (!(slot_min(h, 0, G) > 0.0)) return fail(QPK_E_STATE, "step left the strict interior");
+    rc = ipm_residuals(c, mu, nrm, &finite);
+    if (rc) return rc;
+    if (!finite) return fail(QPK_E_STATE, "non-finite residual encountered");
+    if (trace) {
+      qpk_ipm_trace& tr = trace[it - 1];
+      tr.iter = (int)it; tr.cg_iters = info.iterations; tr.mu = mu;
+      tr.primal_inf = nrm[0]; tr.dual_inf = nrm[1]; tr.compl_inf = nrm[2];
+      tr.cg_resid = info.final_residual_norm; tr.alpha_x = ax; tr.alpha_lam = al;
+    }
+    res->iterations = (int)it;
+    if (cfg->verbose)
+      fprintf(stderr, "iter %4lld  mu %9.3e  primal %9.3e  dual %9.3e  compl %9.3e  cg %5d  alpha (%.3f, %.3f)\n",
+              it, mu, nrm[0], nrm[1], nrm[2], info.iterations, ax, al);
+    // barrier update (ipm.py:166-173, 229-235)
+    if (nrm[3] < mu) {
+      if (mu < cfg->mu_tol) { res->status = 0; break; }
+      mu = mu / cfg->mu_shrink;
+      rc = ipm_residuals(c, mu, nrm, &finite);
+      if (rc) return rc;
+    }
+  }
+  // objective at the final x (residuals left H x in ipm_hx)
+  ipm_hess_apply(c, P.x, P.hx);
+  k_ipm_objective<<<G, QPK_BLOCK, 0, s>>>(P);
+  c->launches++;
+  std::vector<double> h;
+  rc = ipm_read(c, 2, h);
+  if (rc) return rc;
+  res->objective = 0.5 * slot_sum(h, 0, G) + slot_sum(h, 1, G);
+  if (x_out) {
+    CUDA_TRY(cudaMemcpyAsync(x_out, P.x, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  res->wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return QPK_OK;
 }
 
