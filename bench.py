@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--ref-iters-per-step", type=int, default=5)
     ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg5 = headline sweep; cfg1-4 = PCG sweep on the first IPM iteration's operator")
+    ap.add_argument("--ipm", action="store_true",
+                    help="IPM wall time of the device-resident IPM on --workload (cfg1 pinned at mu_tol 1e-8, "
+                         "CG tol 1e-10; others at the reference defaults)")
+    ap.add_argument("--cpu-ipm-iters", type=int, default=0,
+                    help="IPM iterations in the CPU-baseline sample (0 = full solve for cfg1, 2 otherwise)")
     args = ap.parse_args()
     if args.workload != "cfg5" and args.iters == 500:
         args.iters = 200
@@ -367,8 +372,83 @@ def run_ours(args):
         torch.distributed.destroy_process_group()
 
 
+def ipm_problem(name):
+    from paper_2308_00637_b200 import workloads
+    from paper_2308_00637_b200.ipm import IpmConfig
+    from paper_2308_00637_b200.pcg import PcgConfig
+    if name == "cfg1":
+        problem, _, _ = workloads.dense_qp(seed=0)
+        return problem, IpmConfig(mu_tol=1e-8, pcg=PcgConfig(tol=1e-10))
+    if name == "cfg2":
+        problem, _, _ = workloads.svm_primal(seed=2)
+    elif name == "cfg3":
+        problem, _, _ = workloads.rt_like(seed=3)
+    elif name == "cfg4":
+        problem, _, _ = workloads.rt_like(seed=4, n_vox=2_000_000, n_beam=100_000, density=0.001)
+    else:
+        raise SystemExit("--ipm needs --workload cfg1..cfg4 (cfg5 is a fixed-iteration PCG sweep)")
+    return problem, IpmConfig()
+
+
+def run_ipm(args):
+    """IPM wall time: the whole interior-point solve with the device-resident IPM."""
+    import torch
+    from paper_2308_00637_b200.ipm import DeviceIpm, solve as dev_solve
+    rank, world, local = dist_env()
+    if world > 1 and rank != 0:
+        return                       # single-GPU measurement (replicas would be identical)
+    torch.cuda.set_device(local)
+    problem, cfg = ipm_problem(args.workload)
+    dev = DeviceIpm(problem, device=local)
+    launches0 = dev.kkt.ctx.query("kernel_launches")
+    for _ in range(max(args.warmup, 3)):
+        rep = dev.solve(cfg)
+    walls = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            rep = dev.solve(cfg)
+            walls.append(rep.wall_time)
+    launches = (dev.kkt.ctx.query("kernel_launches") - launches0) // (args.steps + max(args.warmup, 3))
+    dev.close()
+    # e2e: problem upload + solve + x back, through the public solve()
+    t0 = time.perf_counter()
+    rep_e2e = dev_solve(problem, cfg, device=local)
+    e2e = time.perf_counter() - t0
+    line = {
+        "metric": "IPM wall time (device-resident IPM + Jacobi-PCG direction solver)", "value": float(np.mean(walls)),
+        "unit": "s", "n_gpus": 1, "steps": args.steps, "warmup": max(args.warmup, 3),
+        "ms_per_step": float(np.mean(walls)) * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded BASELINE generator; no dataset)",
+        "config": {"workload": WORKLOAD_DESC[args.workload], "ipm": {"mu_tol": cfg.mu_tol, "cg_tol": cfg.pcg.tol,
+                   "cg_max_iters": cfg.pcg.max_iters}, "status": rep.status.value, "ipm_iterations": rep.iterations,
+                   "cg_iterations": rep.cg_total, "objective": rep.objective,
+                   "l2": "each step re-solves the resident problem"},
+        "e2e": {"value": e2e, "unit": "s", "h2d_bytes_per_step": None, "d2h_bytes_per_step": 8 * problem.n,
+                "path": "paper_2308_00637_b200.ipm.solve(problem, cfg): upload + solve + x D2H"},
+        "gpu_launches": int(launches), "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        from oracle import qp_oracle as orc
+        k = args.cpu_ipm_iters or (cfg.max_iters if args.workload == "cfg1" else 2)
+        ocfg = orc.IpmConfig(gamma=cfg.gamma, mu_init=cfg.mu_init, mu_tol=cfg.mu_tol, mu_shrink=cfg.mu_shrink,
+                             max_iters=k, pcg=orc.PcgConfig(tol=cfg.pcg.tol, max_iters=cfg.pcg.max_iters))
+        orep = orc.solve(problem, ocfg)
+        full = orep.status == "converged"
+        line["cpu_baseline"] = {
+            "value": orep.wall_time if full else orep.wall_time / max(orep.iterations, 1),
+            "unit": "s" if full else "s per IPM iteration", "cores": 1, "kind": "port",
+            "sample": (f"full CPU IPM ({orep.iterations} IPM / {sum(t['cg_iters'] for t in orep.trace)} CG "
+                       f"iterations, status {orep.status})" if full else
+                       f"first {orep.iterations} IPM iterations ({sum(t['cg_iters'] for t in orep.trace)} CG)")
+                      + "; oracle = numpy/scipy restatement of qpipm, bit-identical on the golden vectors"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.ipm and args.impl != "reference":
+        run_ipm(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:
