@@ -1006,6 +1006,7 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   if (per_sm < 1) return fail(QPK_E_UNSUPPORTED, "PCG kernel cannot be resident");
   const long long work = std::max<long long>((long long)c->h_ci.size() / 1024, N / 512);
   c->grid_pcg = (int)std::max<long long>(1, std::min<long long>((long long)per_sm * c->sms, work));
+  if (const char* ev = getenv("QPK_GRID")) c->grid_pcg = std::max(1, std::min(per_sm * c->sms, atoi(ev)));
   c->grid_std = c->grid_pcg;
   {
     int eng_per_sm = c->scatter == QPK_SCATTER_DICT ? 3 : 4;
