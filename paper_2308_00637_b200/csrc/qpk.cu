@@ -493,15 +493,16 @@ struct qpk_ctx {
   DBuf<double> seg_sum;
   int n_seg = 0, seg_lanes = 8;
   // row-block dictionaries
-  DBuf<int> blk_row, blk_dict, dcols, col_ptr, col_pos, tile_row, blk_tile;
-  DBuf<int4> tile_desc, rtile_desc;
+  DBuf<int> dcols, col_ptr, col_pos;
+  DBuf<TileDescD> tiles;
+  DBuf<double> tval;
+  DBuf<int4> rtile_desc;
   int n_rtiles = 0;
   int tma_rows = -1;              // -1 auto (env QPK_TMA_ROWS)
-  DBuf<unsigned short> lci;
   DBuf<double> bpart;
   int nblk = 0;
   bool have_dict = false;
-  double dict_reuse = 0.0;
+  double dict_reuse = 0.0;        // tile density: nonzeros / dense tile slots
   DBuf<double> bv, cv, hh, hv, hdense, U, w, hdiag;
   bool have_csc = false;
 
@@ -564,7 +565,6 @@ static cudaError_t upload(DBuf<T>& dst, const std::vector<T>& src, cudaStream_t 
   return cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
 
-static constexpr int DICT_SMEM = (1 + QPK_DICT_WARPS) * QPK_DICT_MAX * (int)sizeof(double);
 static int engine_setup(qpk_ctx* c);
 static Engine make_engine(qpk_ctx* c);
 
@@ -822,99 +822,85 @@ static int build_csc(qpk_ctx* c) {
   return QPK_OK;
 }
 
-// Row blocks of <= QPK_DICT_ROWS rows whose distinct columns fit a
-// QPK_DICT_MAX-entry shared-memory dictionary; entries re-indexed to 16 bits.
-// Returns QPK_OK with have_dict = false when a row alone exceeds the limit.
+// Dense row tiles: consecutive rows grouped while (rows x padded distinct
+// columns) fits QPK_TILE_DOUBLES, each tile stored as a dense block over its
+// sorted column list.  have_dict = false when a single row is too wide.
 static int build_dict(qpk_ctx* c) {
   c->have_dict = false;
   const long long n = c->n, m = c->m;
-  std::vector<int> mark(n, -1), local(n, 0);
-  std::vector<int> blk_row(1, 0), blk_dict(1, 0), cols, cur;
-  std::vector<unsigned short> lci(c->h_ci.size(), 0xFFFF);
-  cur.reserve(QPK_DICT_MAX);
-  int blk = 0;
-  long long rows_in = 0;
-  auto close_block = [&](long long r_end) {
-    std::vector<int> order(cur.size());
-    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-    std::sort(order.begin(), order.end(), [&](int a, int b) { return cur[a] < cur[b]; });
-    std::vector<int> newpos(cur.size());
-    for (size_t i = 0; i < order.size(); ++i) newpos[order[i]] = (int)i;
-    for (long long r = blk_row.back(); r < r_end; ++r)
-      for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k)
-        if (c->h_ci[k] >= 0) lci[k] = (unsigned short)newpos[lci[k]];
-    for (int i : order) cols.push_back(cur[i]);
-    blk_dict.push_back((int)cols.size());
-    blk_row.push_back((int)r_end);
-    ++blk;
+  std::vector<int> mark(n, -1), cur;
+  std::vector<TileDescD> tiles;
+  std::vector<int> cols;
+  std::vector<double> tval;
+  cur.reserve(QPK_TILE_DMAX);
+  long long slots = 0;
+  long long r = 0;
+  int tid = 0;
+  auto r4 = [](long long x) { return (x + 3) & ~3LL; };
+  while (r < m) {
+    const long long ra = r;
     cur.clear();
-    rows_in = 0;
-  };
-  for (long long r = 0; r < m; ++r) {
-    int fresh = 0, len = 0;
-    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
-      const int col = c->h_ci[k];
-      if (col < 0) continue;
-      ++len;
-      if (mark[col] != blk) ++fresh;
+    while (r < m) {
+      long long fresh = 0;
+      for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+        const int col = c->h_ci[k];
+        if (col >= 0 && mark[col] != tid) ++fresh;
+      }
+      const long long nd = (long long)cur.size() + fresh, rows = r - ra + 1;
+      if (r4(nd) > QPK_TILE_DMAX || rows * (r4(nd) | 1) > QPK_TILE_DOUBLES || rows > QPK_TILE_ROWS) {
+        if (r == ra) return QPK_OK;                    // one row alone does not fit a tile
+        break;
+      }
+      for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+        const int col = c->h_ci[k];
+        if (col >= 0 && mark[col] != tid) { mark[col] = tid; cur.push_back(col); }
+      }
+      ++r;
     }
-    if (len > QPK_DICT_MAX) return QPK_OK;                 // row too wide for a dictionary
-    if (rows_in > 0 && (rows_in >= QPK_DICT_ROWS || (long long)cur.size() + fresh > QPK_DICT_MAX)) close_block(r);
-    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
-      const int col = c->h_ci[k];
-      if (col < 0) continue;
-      if (mark[col] != blk) { mark[col] = blk; local[col] = (int)cur.size(); cur.push_back(col); }
-      lci[k] = (unsigned short)local[col];
-    }
-    ++rows_in;
+    std::sort(cur.begin(), cur.end());
+    const int ndp = (int)r4((long long)cur.size());
+    const int pitch = ndp | 1;                          // odd row pitch: conflict-free column reads
+    TileDescD td;
+    td.ra = (int)ra; td.rb = (int)r; td.d0 = (int)cols.size(); td.ndp = ndp;
+    td.v0 = (int)((tval.size() + 1) & ~(size_t)1);    // 16-byte aligned block start
+    td.pad0 = pitch; td.pad1 = td.pad2 = 0;
+    if ((long long)td.v0 + (r - ra) * pitch >= (1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "tiles exceed int32");
+    for (int col : cur) cols.push_back(col);
+    for (int i = (int)cur.size(); i < ndp; ++i) cols.push_back(-1);
+    const size_t base = td.v0;
+    tval.resize(base + (size_t)(r - ra) * pitch, 0.0);
+    for (long long rr = ra; rr < r; ++rr)
+      for (int k = c->h_rp[rr]; k < c->h_rp[rr + 1]; ++k) {
+        const int col = c->h_ci[k];
+        if (col < 0) continue;
+        const int pos = (int)(std::lower_bound(cur.begin(), cur.end(), col) - cur.begin());
+        tval[base + (size_t)(rr - ra) * pitch + pos] = c->h_v[k];
+      }
+    slots += (r - ra) * pitch;
+    tiles.push_back(td);
+    ++tid;
   }
-  if (rows_in > 0) close_block(m);
-  // tiles for the TMA pipeline: <= QPK_TILE_E padded entries and <= QPK_TILE_R rows
-  std::vector<int> tile_row, blk_tile(1, 0);
-  for (int b = 0; b < blk; ++b) {
-    int r = blk_row[b];
-    while (r < blk_row[b + 1]) {
-      tile_row.push_back(r);
-      int rows = 0;
-      const int e0 = c->h_rp[r];
-      while (r < blk_row[b + 1] && rows < QPK_TILE_R && c->h_rp[r + 1] - e0 <= QPK_TILE_E - 16) { ++r; ++rows; }
-      if (rows == 0) return QPK_OK;                          // a row wider than a tile
-    }
-    blk_tile.push_back((int)tile_row.size());
-  }
-  tile_row.push_back((int)m);
-  // column -> its dictionary positions, in block order
-  std::vector<int> col_ptr(n + 1, 0), col_pos(cols.size());
-  for (int col : cols) col_ptr[col + 1]++;
+  // column -> its tile-partial positions, in tile order
+  std::vector<int> col_ptr(n + 1, 0), col_pos;
+  for (int col : cols) if (col >= 0) col_ptr[col + 1]++;
   for (long long j = 0; j < n; ++j) col_ptr[j + 1] += col_ptr[j];
+  col_pos.resize(col_ptr[n]);
   {
     std::vector<int> at(col_ptr.begin(), col_ptr.end() - 1);
-    for (size_t p = 0; p < cols.size(); ++p) col_pos[at[cols[p]]++] = (int)p;
+    for (size_t p = 0; p < cols.size(); ++p) if (cols[p] >= 0) col_pos[at[cols[p]]++] = (int)p;
   }
+  cols.resize(cols.size() + 16, -1);                  // bulk copies read 16-byte windows
+  tval.resize(tval.size() + 16, 0.0);
   cudaStream_t s = c->stream;
-  CUDA_TRY(upload(c->blk_row, blk_row, s));
-  CUDA_TRY(upload(c->blk_dict, blk_dict, s));
+  CUDA_TRY(upload(c->tiles, tiles, s));
   CUDA_TRY(upload(c->dcols, cols, s));
+  CUDA_TRY(upload(c->tval, tval, s));
   CUDA_TRY(upload(c->col_ptr, col_ptr, s));
   CUDA_TRY(upload(c->col_pos, col_pos, s));
-  CUDA_TRY(upload(c->tile_row, tile_row, s));
-  CUDA_TRY(upload(c->blk_tile, blk_tile, s));
-  {
-    std::vector<int4> td(tile_row.size() - 1);
-    for (size_t t = 0; t + 1 < tile_row.size(); ++t)
-      td[t] = make_int4(tile_row[t], tile_row[t + 1], c->h_rp[tile_row[t]], c->h_rp[tile_row[t + 1]]);
-    CUDA_TRY(upload(c->tile_desc, td, s));
-  }
-  {
-    // bulk copies may over-read a few aligned elements past the end
-    std::vector<unsigned short> pad = lci;
-    pad.resize(lci.size() + 32, 0xFFFF);
-    CUDA_TRY(upload(c->lci, pad, s));
-  }
   CUDA_TRY(c->bpart.alloc(std::max<size_t>(cols.size(), 1)));
   CUDA_TRY(cudaStreamSynchronize(s));
-  c->nblk = blk;
-  c->dict_reuse = cols.empty() ? 0.0 : (double)c->nnz / (double)cols.size();
+  c->nblk = tid;
+  c->dict_reuse = slots ? (double)c->nnz / (double)slots : 0.0;
   c->have_dict = true;
   return QPK_OK;
 }
@@ -990,8 +976,15 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   if ((scatter == QPK_SCATTER_AUTO || scatter == QPK_SCATTER_DICT) && c->m > 0) {
     int rc = build_dict(c);
     if (rc) return rc;
-    if (c->have_dict && scatter == QPK_SCATTER_DICT) c->scatter = QPK_SCATTER_DICT;
-    else if (scatter == QPK_SCATTER_DICT || (c->have_dict && c->dict_reuse >= 4.0)) scatter = QPK_SCATTER_CSC;
+    // Dense tiles pay off when they are mostly nonzeros (banded / clustered
+    // B: RT, SVM, dense).  Such B makes fp64 atomics contend, so small
+    // systems of that kind take the CSC gather (in the single-launch
+    // persistent kernel) instead; random B (cfg5) keeps the one-pass atomics.
+    const bool dense_tiles = c->have_dict && c->dict_reuse >= 0.5;
+    if (c->have_dict && (scatter == QPK_SCATTER_DICT || (dense_tiles && c->N() >= 50000)))
+      c->scatter = QPK_SCATTER_DICT;
+    else if (scatter == QPK_SCATTER_DICT || dense_tiles)
+      scatter = QPK_SCATTER_CSC;
   }
   if (scatter == QPK_SCATTER_CSC && c->m > 0) {
     int rc = build_csc(c);
@@ -1068,16 +1061,12 @@ static int build_jacobi(qpk_ctx* c) {
     int rc = engine_setup(c);
     if (rc) return rc;
     Engine E = make_engine(c);
-    k_jac_dict<<<c->grid_eng, QPK_DICT_WARPS * 32, DICT_SMEM, s>>>(E);
-    if (c->sharded) {
-      // local column sums, summed over ranks, then the common finish
-      k_dict_col_sum<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p);
-      int rc2 = allreduce_sum(c, c->y.p, c->n, s);
-      if (rc2) return rc2;
-      k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
-    } else {
-      k_jac_dict_finish<<<G, QPK_BLOCK, 0, s>>>(E, c->hdiag.p, c->jac.p, c->minv.p);
-    }
+    k_jac_tile<<<c->grid_eng, QPK_BLOCK, 0, s>>>(E);
+    // column sums of the tile partials (sharded: summed over ranks), then the common finish
+    k_tile_combine<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 0, -1);
+    int rc2 = allreduce_sum(c, c->y.p, c->n, s);
+    if (rc2) return rc2;
+    k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
     c->launches += 2;
     CUDA_TRY(cudaGetLastError());
     c->jac_ready = true;
@@ -1177,11 +1166,10 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   const int G = c->grid_eng;
   k_slot_top<<<G, QPK_BLOCK, 0, s>>>(E, par);
   if (c->scatter == QPK_SCATTER_DICT) {
-    Tiles T;
-    T.tile_row = c->tile_row.p;
-    T.blk_tile = c->blk_tile.p;
-    T.tile_desc = c->tile_desc.p;
-    k_slot_rows_tma<<<E.G_rows, (QPK_DICT_WARPS + 1) * 32, sizeof(TmaSmem), s>>>(E, T, par);
+    k_slot_rows_tile<<<E.G_rows, (QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32,
+                       sizeof(DTileSmem), s>>>(E, par);
+    k_tile_combine<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);   // y_top += B'z (tile partials)
+    if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
   } else {
     switch (c->lanes * 2 + (csc ? 1 : 0)) {
       case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
@@ -1200,16 +1188,14 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   }
   if (!c->sharded) {
-    if (c->scatter == QPK_SCATTER_DICT) k_slot_update<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
-    else if (csc) k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
+    if (csc) k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
     else k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
     return;
   }
   // sharded: finish the local top block and scalars, one grouped all-reduce
   // of [y_top | scalars], the update on the now-global y, an all-reduce of
   // r'r and r'z, and the control decision.
-  if (c->scatter == QPK_SCATTER_DICT) k_shard_reduce<3><<<G, QPK_BLOCK, 0, s>>>(E, par);
-  else if (csc) k_shard_reduce<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  if (csc) k_shard_reduce<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
   else k_shard_reduce<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
   nccl().groupStart();
   allreduce_sum(c, c->y.p, c->n, s);
@@ -1234,16 +1220,15 @@ static Engine make_engine(qpk_ctx* c) {
   E.scatter = c->scatter;
   E.sharded = c->sharded ? 1 : 0;
   E.gscal = c->gscal.p; E.lscal2 = c->lscal2.p; E.abuf = c->abuf.p;
-  E.dict.nblk = c->nblk; E.dict.blk_row = c->blk_row.p; E.dict.blk_dict = c->blk_dict.p; E.dict.cols = c->dcols.p;
-  E.dict.lci = c->lci.p; E.dict.bpart = c->bpart.p; E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
+  E.dict.nblk = c->nblk; E.dict.tiles = c->tiles.p; E.dict.cols = c->dcols.p; E.dict.tval = c->tval.p;
+  E.dict.bpart = c->bpart.p; E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
   return E;
 }
 
 static int engine_setup(qpk_ctx* c) {
   if (c->ctrl.p) return QPK_OK;
-  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(k_jac_dict, cudaFuncAttributeMaxDynamicSharedMemorySize, DICT_SMEM));
-  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(TmaSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sizeof(DTileSmem)));
   CUDA_TRY(c->ctrl.alloc(2));
   CUDA_TRY(c->gscal.alloc(4));
   CUDA_TRY(c->lscal2.alloc(2));
@@ -1674,7 +1659,7 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "world") return c->world;
   if (k == "rank") return c->rank;
   if (k == "dict_blocks") return c->nblk;
-  if (k == "dict_reuse_x100") return (int64_t)(c->dict_reuse * 100);
+  if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "block") return QPK_BLOCK;
   if (k == "sms") return c->sms;
   if (k == "hess_kind") return c->hkind;

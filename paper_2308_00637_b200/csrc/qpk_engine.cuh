@@ -39,23 +39,27 @@ struct EngineCfg {
   double* hist;       // nullable, max_iters + 1
 };
 
-#ifndef QPK_DICT_MAX
-#define QPK_DICT_MAX 1024        // distinct columns per row block
-#endif
-#define QPK_DICT_WARPS 8         // warps per CTA in the dictionary kernels
-#define QPK_DICT_ROWS 512        // rows per block (at most)
+#define QPK_TILE_DOUBLES 4096     // a dense tile holds <= 4096 values (32 KB)
+#define QPK_TILE_ROWS 64
+#define QPK_TILE_DMAX 1024        // distinct columns per tile
 
-// Row-block dictionaries: rows [blk_row[b], blk_row[b+1]) touch the sorted
-// global columns cols[blk_dict[b] .. blk_dict[b+1]); lci holds each B entry's
-// index into its block's dictionary (0xFFFF = padding).  bpart[p] is block b's
-// partial of (B'z) for dictionary position p; col_pos[col_ptr[j] ..
-// col_ptr[j+1]) lists column j's positions in block order.
+// Dense row tiles (the "dictionary" mode): tile t covers rows [ra, rb) of B
+// and its ndp (multiple of 4) distinct columns cols[d0 .. d0+ndp) (-1 pads);
+// its entries are stored as a dense row-major (rb-ra) x ndp block at
+// tval[v0 ..] -- banded / clustered B is 85-100 % dense inside such a tile,
+// so no per-entry index is needed (~8-9 B per nonzero instead of 12).
+// bpart[d0 + c] is the tile's partial of (B'z) for its column c;
+// col_pos[col_ptr[j] .. col_ptr[j+1]) lists column j's bpart positions in
+// tile order (deterministic combination).
+struct TileDescD {
+  int ra, rb, d0, ndp, v0, pad0, pad1, pad2;
+};
+
 struct Dict {
-  int nblk;
-  const int* blk_row;
-  const int* blk_dict;
+  int nblk;                 // number of tiles
+  const TileDescD* tiles;
   const int* cols;
-  const unsigned short* lci;
+  const double* tval;
   double* bpart;
   const int* col_ptr;
   const int* col_pos;
@@ -283,130 +287,6 @@ __device__ __forceinline__ double top_value(const Engine& E, int j) {
     for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
   }
   return E.y[j] + s;
-}
-
-// ------------------------------------------------------------- dictionary ----
-// One pass over B with no atomics: a CTA takes a row block, stages u[dict]
-// in shared memory, and each warp processes one row at a time (32 lanes,
-// distinct columns), gathering u from shared memory and accumulating z B_r
-// into its own shared-memory copy of the block's dictionary.  The 8 copies
-// are summed in a fixed order into bpart (one value per block and column).
-template <int MODE_JAC>
-__device__ __forceinline__ void dict_rows(const Engine& E, double* v, const RowFuse& f, bool fuse,
-                                          double* sm, double& pacc, double& rzb) {
-  const Op& op = E.op;
-  const Dict& D = E.dict;
-  const double* u = v;
-  double* w = v + op.n;
-  double* us = sm;
-  double* acc = sm + QPK_DICT_MAX;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* aw = acc + warp * QPK_DICT_MAX;
-  for (int blk = blockIdx.x; blk < D.nblk; blk += gridDim.x) {
-    const int r0 = __ldg(D.blk_row + blk), r1 = __ldg(D.blk_row + blk + 1);
-    const int d0 = __ldg(D.blk_dict + blk), nd = __ldg(D.blk_dict + blk + 1) - d0;
-    for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-      if (!MODE_JAC) us[k] = u[__ldg(D.cols + d0 + k)];
-#pragma unroll
-      for (int ww = 0; ww < QPK_DICT_WARPS; ++ww) acc[ww * QPK_DICT_MAX + k] = 0.0;
-    }
-    __syncthreads();
-    for (int r = r0 + warp; r < r1; r += QPK_DICT_WARPS) {
-      const int b = __ldg(op.rp + r), e = __ldg(op.rp + r + 1);
-      const double dr = __ldg(op.d + r);
-      unsigned short li[4];
-      double vv[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = b + lane + 32 * q;
-        li[q] = 0xFFFF;
-        vv[q] = 0.0;
-        if (k < e) { li[q] = __ldg(D.lci + k); vv[q] = __ldg(op.bv + k); }
-      }
-      double z;
-      if (MODE_JAC) {
-        z = 1.0 / dr;                                   // Jacobi: sum_r B_rj^2 / d_r
-      } else {
-        double wr = w[r];
-        double s = 0.0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) if (li[q] != 0xFFFF) s = fma(vv[q], us[li[q]], s);
-        for (int k = b + lane + 128; k < e; k += 32) {
-          const unsigned short l = __ldg(D.lci + k);
-          if (l != 0xFFFF) s = fma(__ldg(op.bv + k), us[l], s);
-        }
-        const double t = subwarp_sum<32>(s);
-        if (fuse) {
-          const double rres = f.r[op.n + r];
-          const double zr = __dmul_rn(1.0 / dr, rres);
-          if (f.xupd && lane == 0) f.xdst[op.n + r] = __dadd_rn(f.xsrc[op.n + r], __dmul_rn(f.alpha_prev, wr));
-          const double pn = f.restart ? zr : __dadd_rn(zr, __dmul_rn(f.beta, wr));
-          if (lane == 0) { w[r] = pn; rzb += rres * zr; }
-          wr = pn;
-        }
-        z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
-        const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
-        if (lane == 0) {
-          E.y[op.n + r] = yb;
-          pacc += t * z + wr * yb;
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (li[q] != 0xFFFF) aw[li[q]] += MODE_JAC ? __dmul_rn(vv[q], vv[q]) * z : z * vv[q];
-      for (int k = b + lane + 128; k < e; k += 32) {
-        const unsigned short l = __ldg(D.lci + k);
-        if (l != 0xFFFF) {
-          const double a = __ldg(op.bv + k);
-          aw[l] += MODE_JAC ? __dmul_rn(a, a) * z : z * a;
-        }
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < nd; k += blockDim.x) {
-      double s = 0.0;
-#pragma unroll
-      for (int ww = 0; ww < QPK_DICT_WARPS; ++ww) s += acc[ww * QPK_DICT_MAX + k];
-      D.bpart[d0 + k] = s;
-    }
-    __syncthreads();
-  }
-}
-
-__global__ void __launch_bounds__(QPK_DICT_WARPS * 32, 3) k_slot_rows_dict(Engine E, int par) {
-  extern __shared__ double sm[];
-  __shared__ double red[32];
-  __shared__ double s_lr[QPK_KMAX];
-  const Ctrl c = E.ctrl[par];
-  if (c.mode == MODE_DONE) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_rows = globaltimer_ns();
-  const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
-  RowFuse f{};
-  double* v;
-  if (fuse) {
-    f.r = E.r; f.xsrc = E.x[c.cur]; f.xdst = E.x[c.xn];
-    f.alpha_prev = c.alpha_prev; f.beta = c.beta;
-    f.restart = c.mode == MODE_RESTART; f.xupd = c.xupd;
-    v = E.p;
-  } else {
-    v = E.x[c.mode == MODE_CHECK ? c.xn : c.best];
-  }
-  double pacc = 0.0, rzb = 0.0;
-  dict_rows<0>(E, v, f, fuse, sm, pacc, rzb);
-  pacc += hess_rows(E.op, v, E.y, E.part, E.G, red, s_lr);
-  double t = block_sum(pacc, red);
-  if (threadIdx.x == 0) E.part[SLOT_ROWS * E.G + blockIdx.x] = t;
-  t = block_sum(rzb, red);
-  if (threadIdx.x == 0) E.part[SLOT_AUX2 * E.G + blockIdx.x] = t;
-}
-
-// Jacobi through the dictionaries (deterministic): bpart <- sum_r B_rj^2 / d_r
-__global__ void __launch_bounds__(QPK_DICT_WARPS * 32, 3) k_jac_dict(Engine E) {
-  extern __shared__ double sm[];
-  RowFuse f{};
-  double pacc = 0.0, rzb = 0.0;
-  dict_rows<1>(E, nullptr, f, false, sm, pacc, rzb);
 }
 
 // jac_top = (diag(H) + q) + 2 sum of the column's partials ; bottom = D

@@ -1,16 +1,9 @@
-// qpk_tma.cuh -- TMA-fed row-block dictionary kernel (the one-pass, atomic-
-// free operator apply for banded / clustered B: the RT and SVM configs).
-//
-// Per CTA: 1 producer warp + QPK_DICT_WARPS consumer warps.  The producer's
-// elected lane streams, tile by tile, the tile's 16-bit dictionary indices and
-// fp64 values of B, its row pointers and the per-row vectors it needs (d, w =
-// p_B or x_B, r_B, x_B) from HBM into a QPK_TMA_STAGES-deep ring of shared-
-// memory stages with 1-D bulk async copies (cp.async.bulk ... complete_tx on
-// an mbarrier; SASS UBLKCP).  Consumers wait on the stage's "full" barrier,
-// process the rows from shared memory (u gathered from the block's
-// dictionary copy in shared memory, B'z accumulated into per-warp shared-
-// memory dictionaries, no atomics), and release the stage on its "empty"
-// barrier.  Only the per-row outputs go back to HBM.
+// qpk_tma.cuh -- TMA-fed kernels: 1-D bulk async copies (cp.async.bulk ...
+// mbarrier::complete_tx; SASS UBLKCP) from HBM into a ring of shared-memory
+// stages, filled by one producer lane and drained by consumer warps.
+//   k_slot_rows_tile     dense-tile apply for clustered B (one pass, no atomics)
+//   k_slot_rows_tma_csr  CSR apply with the indices staged in shared memory
+//                        (experimental; QPK_TMA_ROWS=1)
 #pragma once
 #include "qpk_engine.cuh"
 
@@ -50,54 +43,74 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void consumer_bar() {
-  asm volatile("bar.sync 1, %0;" ::"r"(QPK_DICT_WARPS * 32) : "memory");
-}
 
 // tile descriptor written by the producer into its stage (visible to the
 // consumers through the mbarrier's release/acquire)
 struct TileDesc {
   int ra, rb;           // rows
-  int e0;               // first entry copied for lci (multiple of 8)
+  int e0;               // first entry copied for indices
   int e1;               // first entry copied for values (multiple of 2)
   int p0;               // first row pointer copied (multiple of 4)
   int v0;               // first row copied for d (multiple of 2)
   int w0;               // first element copied of the bottom vectors (n + row, multiple of 2)
 };
 
-struct alignas(16) TileStage {
-  unsigned short lci[QPK_TILE_E + 16];
-  double val[QPK_TILE_E + 8];
-  int rp[QPK_TILE_R + 8];
-  double d[QPK_TILE_R + 4];
-  double w[QPK_TILE_R + 4];
-  double r[QPK_TILE_R + 4];
-  double x[QPK_TILE_R + 4];
-  TileDesc t;
+__device__ __forceinline__ uint32_t round_up16(uint32_t b) { return b == 0u ? 16u : (b + 15u) & ~15u; }
+
+// ---------------------------------------------------------------------------
+// Dense-tile kernel (the one-pass, atomic-free apply for clustered B).
+// Producer warp: one elected lane streams each tile's dense block, its
+// column list and the tile's per-row vectors into a 4-stage ring with
+// cp.async.bulk (UBLKCP) + mbarrier complete_tx.  Consumers (8 warps):
+//   u_dict[c] = u[cols[c]]  (gathered one tile ahead, from registers)
+//   rows:    t_r = A_r . u_dict  (warp per row), z_r, y_B, fused bottom update
+//   columns: bpart[c] = sum_r A[r][c] z_r  (thread per column, no atomics)
+#define QPK_TILE_WARPS 8
+#define QPK_TILE_STAGES 4
+
+struct alignas(16) DTileStage {
+  double a[QPK_TILE_DOUBLES + 2];
+  double ud[QPK_TILE_DMAX];        // u[cols], gathered by the gather warp
+  int cols[QPK_TILE_DMAX];
+  double d[QPK_TILE_ROWS + 4];
+  double w[QPK_TILE_ROWS + 4];
+  double r[QPK_TILE_ROWS + 4];
+  double x[QPK_TILE_ROWS + 4];
+  TileDescD t;
+  int v0, w0, pad0, pad1;
 };
 
-struct TmaSmem {
-  TileStage st[QPK_TMA_STAGES];
-  unsigned long long full[QPK_TMA_STAGES], empty[QPK_TMA_STAGES];
-  double us[QPK_DICT_MAX];
-  double acc[QPK_DICT_WARPS][QPK_DICT_MAX];
+#ifndef QPK_TILE_GROUPS
+#define QPK_TILE_GROUPS 2        // consumer groups working on alternate tiles
+#endif
+#define QPK_TILE_GWARPS 4        // warps per consumer group
+#define QPK_TILE_GATHER_WARPS 2  // warps gathering u[cols] for landed tiles
+
+struct DTileSmem {
+  DTileStage st[QPK_TILE_STAGES];
+  unsigned long long full[QPK_TILE_STAGES], empty[QPK_TILE_STAGES], uready[QPK_TILE_STAGES];
+  double rpart[QPK_TILE_GROUPS][QPK_TILE_GWARPS][QPK_TILE_ROWS];
+  double zs[QPK_TILE_GROUPS][QPK_TILE_ROWS];
   double red[32];
   double s_lr[QPK_KMAX];
 };
 
-// tiles of the row blocks: tile t covers rows [tile_row[t], tile_row[t+1]);
-// block b owns tiles [blk_tile[b], blk_tile[b+1])
-struct Tiles {
-  const int* tile_row;
-  const int* blk_tile;
-  const int4* tile_desc;      // (first row, end row, first entry, end entry) per tile
-};
+__device__ __forceinline__ void tile_group_bar(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "r"(QPK_TILE_GWARPS * 32) : "memory");
+}
 
-__device__ __forceinline__ uint32_t round_up16(uint32_t b) { return b == 0u ? 16u : (b + 15u) & ~15u; }
-
-__global__ void __launch_bounds__((QPK_DICT_WARPS + 1) * 32, 1) k_slot_rows_tma(Engine E, Tiles T, int par) {
+// Tile layout: rows of the dense block have an odd pitch (ndp | 1 doubles,
+// TileDescD::pad0) so that 32 lanes reading one column of consecutive rows
+// hit distinct banks.  QPK_TILE_GROUPS groups of QPK_TILE_GWARPS consumer
+// warps take alternate tiles (so one group's barrier-separated passes overlap
+// another's); per tile a group runs three regular shared-memory passes: row
+// slices (warp w, lane = row), row finish (thread per row), columns (thread
+// per column).
+__global__ void __launch_bounds__((QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32, 1)
+k_slot_rows_tile(Engine E, int par) {
   extern __shared__ __align__(128) unsigned char smraw[];
-  TmaSmem& S = *reinterpret_cast<TmaSmem*>(smraw);
+  DTileSmem& S = *reinterpret_cast<DTileSmem*>(smraw);
+  constexpr int CW = QPK_TILE_GROUPS * QPK_TILE_GWARPS;   // consumer warps
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_rows = globaltimer_ns();
@@ -107,181 +120,191 @@ __global__ void __launch_bounds__((QPK_DICT_WARPS + 1) * 32, 1) k_slot_rows_tma(
   const Dict& D = E.dict;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < QPK_TMA_STAGES; ++s) {
+    for (int s = 0; s < QPK_TILE_STAGES; ++s) {
       mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], QPK_DICT_WARPS);
+      mbar_init(&S.uready[s], 1);
+      mbar_init(&S.empty[s], QPK_TILE_GWARPS);       // a stage is drained by one group
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
+  const int my = (D.nblk > (int)blockIdx.x) ? (D.nblk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   double pacc = 0.0, rzb = 0.0;
-  if (warp == QPK_DICT_WARPS) {
+  if (warp == CW) {
     // ---------------------------------------------------------- producer ----
-    // The whole warp fetches the tile descriptors of a block (lane i holds
-    // tile t0 + i) one block ahead; lane 0 issues the bulk copies.
-    int it = 0;
-    const double* wsrc = v;                          // bottom vector w lives at v[n + r]
-    const double* xsrc = E.x[c.cur];
-    int blk = blockIdx.x;
-    int t0 = 0, t1 = 0;
-    int4 dsc = make_int4(0, 0, 0, 0);
-    if (blk < D.nblk) {
-      t0 = __ldg(T.blk_tile + blk); t1 = __ldg(T.blk_tile + blk + 1);
-      if (t0 + lane < t1) dsc = __ldg(T.tile_desc + t0 + lane);
-    }
-    while (blk < D.nblk) {
-      // prefetch the next block's descriptors
-      const int nblk2 = blk + gridDim.x;
-      int u0 = 0, u1 = 0;
-      int4 ndsc = make_int4(0, 0, 0, 0);
-      if (nblk2 < D.nblk) {
-        u0 = __ldg(T.blk_tile + nblk2); u1 = __ldg(T.blk_tile + nblk2 + 1);
-        if (u0 + lane < u1) ndsc = __ldg(T.tile_desc + u0 + lane);
-      }
-      for (int tb = t0; tb < t1; tb += 32) {
-        if (tb != t0) dsc = (tb + lane < t1) ? __ldg(T.tile_desc + tb + lane) : make_int4(0, 0, 0, 0);
-        const int cnt = min(32, t1 - tb);
-        for (int i = 0; i < cnt; ++i, ++it) {
-          const int ra = __shfl_sync(0xffffffffu, dsc.x, i), rb = __shfl_sync(0xffffffffu, dsc.y, i);
-          const int ea = __shfl_sync(0xffffffffu, dsc.z, i), eb = __shfl_sync(0xffffffffu, dsc.w, i);
-          const int s = it % QPK_TMA_STAGES;
-          const uint32_t ph = (it / QPK_TMA_STAGES) & 1;
-          mbar_wait(&S.empty[s], ph ^ 1);
-          if (lane == 0) {
-            TileStage& st = S.st[s];
-            TileDesc td;
-            td.ra = ra; td.rb = rb;
-            td.e0 = ea & ~7;
-            td.e1 = ea & ~1;
-            td.p0 = ra & ~3;
-            td.v0 = ra & ~1;
-            td.w0 = (op.n + ra) & ~1;
-            st.t = td;
-            const uint32_t b_lci = round_up16((uint32_t)(((eb + 7) & ~7) - td.e0) * 2u);
-            const uint32_t b_val = round_up16((uint32_t)(((eb + 1) & ~1) - td.e1) * 8u);
-            const uint32_t b_rp = round_up16((uint32_t)(((rb + 1 + 3) & ~3) - td.p0) * 4u);
-            const uint32_t b_d = round_up16((uint32_t)(((rb + 1) & ~1) - td.v0) * 8u);
-            const uint32_t b_w = round_up16((uint32_t)(((op.n + rb + 1) & ~1) - td.w0) * 8u);
-            const uint32_t bytes = b_lci + b_val + b_rp + b_d + b_w + (fuse ? 2 * b_w : 0u);
-            mbar_expect_tx(&S.full[s], bytes);
-            bulk_g2s(st.lci, D.lci + td.e0, b_lci, &S.full[s]);
-            bulk_g2s(st.val, op.bv + td.e1, b_val, &S.full[s]);
-            bulk_g2s(st.rp, op.rp + td.p0, b_rp, &S.full[s]);
-            bulk_g2s(st.d, op.d + td.v0, b_d, &S.full[s]);
-            bulk_g2s(st.w, wsrc + td.w0, b_w, &S.full[s]);
-            if (fuse) {
-              bulk_g2s(st.r, E.r + td.w0, b_w, &S.full[s]);
-              bulk_g2s(st.x, xsrc + td.w0, b_w, &S.full[s]);
-            }
-          }
-          __syncwarp();
+    if (lane == 0) {
+      const double* wsrc = v;
+      const double* xsrc = E.x[c.cur];
+      for (int it = 0; it < my; ++it) {
+        const int t = blockIdx.x + it * gridDim.x;
+        const int s = it % QPK_TILE_STAGES;
+        mbar_wait(&S.empty[s], ((it / QPK_TILE_STAGES) & 1) ^ 1);
+        DTileStage& st = S.st[s];
+        const TileDescD td = D.tiles[t];
+        st.t = td;
+        const int v0 = td.ra & ~1, w0 = (op.n + td.ra) & ~1;
+        st.v0 = v0;
+        st.w0 = w0;
+        const uint32_t b_a = round_up16((uint32_t)((td.rb - td.ra) * td.pad0) * 8u);
+        const uint32_t b_c = round_up16((uint32_t)td.ndp * 4u);
+        const uint32_t b_d = round_up16((uint32_t)(((td.rb + 1) & ~1) - v0) * 8u);
+        const uint32_t b_w = round_up16((uint32_t)(((op.n + td.rb + 1) & ~1) - w0) * 8u);
+        mbar_expect_tx(&S.full[s], b_a + b_c + b_d + b_w + (fuse ? 2 * b_w : 0u));
+        bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
+        bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
+        bulk_g2s(st.d, op.d + v0, b_d, &S.full[s]);
+        bulk_g2s(st.w, wsrc + w0, b_w, &S.full[s]);
+        if (fuse) {
+          bulk_g2s(st.r, E.r + w0, b_w, &S.full[s]);
+          bulk_g2s(st.x, xsrc + w0, b_w, &S.full[s]);
         }
       }
-      blk = nblk2; t0 = u0; t1 = u1; dsc = ndsc;
+    }
+  } else if (warp > CW) {
+    // ----------------------------------------------------- gather warps ----
+    // u[cols] for each landed tile (warp CW+1+k takes tiles it = k mod NGW),
+    // 8 independent gathers in flight per lane, then "u ready"
+    constexpr int NGW = QPK_TILE_GATHER_WARPS;
+    const double* u = v;
+    for (int it = warp - CW - 1; it < my; it += NGW) {
+      const int s = it % QPK_TILE_STAGES;
+      mbar_wait(&S.full[s], (it / QPK_TILE_STAGES) & 1);
+      DTileStage& st = S.st[s];
+      const int nd = st.t.ndp;
+      for (int cb = lane; cb < nd; cb += 32 * 8) {
+        double g8[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int cc = cb + 32 * q;
+          const int col = cc < nd ? st.cols[cc] : -1;
+          g8[q] = col >= 0 ? u[col] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int cc = cb + 32 * q;
+          if (cc < nd) st.ud[cc] = g8[q];
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.uready[s]);
     }
   } else {
     // ---------------------------------------------------------- consumers ---
-    const double* u = v;
-    double* w = v + op.n;
-    double* aw = S.acc[warp];
-    const int ctid = threadIdx.x;                    // 0 .. 32*W-1
-    int it = 0;
-    for (int blk = blockIdx.x; blk < D.nblk; blk += gridDim.x) {
-      const int d0 = __ldg(D.blk_dict + blk), nd = __ldg(D.blk_dict + blk + 1) - d0;
-      for (int k = ctid; k < nd; k += QPK_DICT_WARPS * 32) {
-        S.us[k] = u[__ldg(D.cols + d0 + k)];
-#pragma unroll
-        for (int ww = 0; ww < QPK_DICT_WARPS; ++ww) S.acc[ww][k] = 0.0;
-      }
-      consumer_bar();
-      const int t0 = __ldg(T.blk_tile + blk), t1 = __ldg(T.blk_tile + blk + 1);
-      for (int t = t0; t < t1; ++t, ++it) {
-        const int s = it % QPK_TMA_STAGES;
-        const uint32_t ph = (it / QPK_TMA_STAGES) & 1;
-        mbar_wait(&S.full[s], ph);
-        const TileStage& st = S.st[s];
-        const TileDesc td = st.t;
-        // RB rows per warp step, their gathers/reductions interleaved for ILP;
-        // the scatters run one row after the other (lanes of a row hold
-        // distinct columns, so the plain read-modify-write is race-free)
-        constexpr int RB = 4;
-        for (int r0 = td.ra + warp; r0 < td.rb; r0 += RB * QPK_DICT_WARPS) {
-          int b[RB], e[RB];
-          double dr[RB], wr[RB], sacc[RB];
-          int tmax = 0;
-#pragma unroll
-          for (int q = 0; q < RB; ++q) {
-            const int r = r0 + q * QPK_DICT_WARPS;
-            b[q] = 0; e[q] = 0; dr[q] = 1.0; wr[q] = 0.0; sacc[q] = 0.0;
-            if (r < td.rb) {
-              b[q] = st.rp[r - td.p0]; e[q] = st.rp[r + 1 - td.p0];
-              dr[q] = st.d[r - td.v0];
-              wr[q] = st.w[op.n + r - td.w0];
-              tmax = max(tmax, e[q] - b[q]);
-            }
+    constexpr int T = QPK_TILE_GWARPS * 32;          // threads per group
+    const int g = warp / QPK_TILE_GWARPS, gw = warp % QPK_TILE_GWARPS;
+    const int tid = threadIdx.x - g * T;
+    double* wv = v + op.n;
+    for (int it = g; it < my; it += QPK_TILE_GROUPS) {
+      const int s = it % QPK_TILE_STAGES;
+      mbar_wait(&S.uready[s], (it / QPK_TILE_STAGES) & 1);
+      const DTileStage& st = S.st[s];
+      const TileDescD td = st.t;
+      const int nd = td.ndp, pitch = td.pad0, R = td.rb - td.ra;
+      const double* ud = st.ud;
+      {
+        const int cs = (nd + QPK_TILE_GWARPS - 1) / QPK_TILE_GWARPS;
+        const int c0 = gw * cs, c1 = min(nd, c0 + cs);
+        for (int rr = lane; rr < R; rr += 32) {
+          const double* arow = st.a + rr * pitch;
+          double s0 = 0.0, s1 = 0.0;
+          int cc = c0;
+          for (; cc + 1 < c1; cc += 2) {
+            s0 = fma(arow[cc], ud[cc], s0);
+            s1 = fma(arow[cc + 1], ud[cc + 1], s1);
           }
-          for (int j = lane; j < tmax; j += 32) {
-#pragma unroll
-            for (int q = 0; q < RB; ++q) {
-              const int k = b[q] + j;
-              if (k < e[q]) {
-                const unsigned short l = st.lci[k - td.e0];
-                if (l != 0xFFFF) sacc[q] = fma(st.val[k - td.e1], S.us[l], sacc[q]);
-              }
-            }
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-            for (int q = 0; q < RB; ++q) sacc[q] += __shfl_xor_sync(0xffffffffu, sacc[q], o);
-#pragma unroll
-          for (int q = 0; q < RB; ++q) {
-            const int r = r0 + q * QPK_DICT_WARPS;
-            if (r >= td.rb) break;
-            const double tt = sacc[q];
-            double wv = wr[q];
-            if (fuse) {
-              const double rres = st.r[op.n + r - td.w0];
-              const double zr = __dmul_rn(1.0 / dr[q], rres);
-              if (c.xupd && lane == 0)
-                E.x[c.xn][op.n + r] = __dadd_rn(st.x[op.n + r - td.w0], __dmul_rn(c.alpha_prev, wv));
-              const double pn = (c.mode == MODE_RESTART) ? zr : __dadd_rn(zr, __dmul_rn(c.beta, wv));
-              if (lane == 0) { w[r] = pn; rzb += rres * zr; }
-              wv = pn;
-            }
-            const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, tt), dr[q]), wv);
-            const double yb = __dadd_rn(tt, __dmul_rn(dr[q], wv));
-            if (lane == 0) {
-              E.y[op.n + r] = yb;
-              pacc += tt * z + wv * yb;
-            }
-            for (int k = b[q] + lane; k < e[q]; k += 32) {
-              const unsigned short l = st.lci[k - td.e0];
-              if (l != 0xFFFF) aw[l] += z * st.val[k - td.e1];
-            }
-            __syncwarp();
-          }
+          if (cc < c1) s0 = fma(arow[cc], ud[cc], s0);
+          S.rpart[g][gw][rr] = s0 + s1;
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[s]);
       }
-      consumer_bar();
-      for (int k = ctid; k < nd; k += QPK_DICT_WARPS * 32) {
-        double sum = 0.0;
+      tile_group_bar(g);
+      for (int rr = tid; rr < R; rr += T) {
+        double tt = 0.0;
 #pragma unroll
-        for (int ww = 0; ww < QPK_DICT_WARPS; ++ww) sum += S.acc[ww][k];
-        D.bpart[d0 + k] = sum;
+        for (int ww = 0; ww < QPK_TILE_GWARPS; ++ww) tt += S.rpart[g][ww][rr];
+        const int r = td.ra + rr;
+        const double dr = st.d[r - st.v0];
+        double wr = st.w[op.n + r - st.w0];
+        if (fuse) {
+          const double rres = st.r[op.n + r - st.w0];
+          const double zr = __dmul_rn(1.0 / dr, rres);
+          if (c.xupd) E.x[c.xn][op.n + r] = __dadd_rn(st.x[op.n + r - st.w0], __dmul_rn(c.alpha_prev, wr));
+          const double pn = (c.mode == MODE_RESTART) ? zr : __dadd_rn(zr, __dmul_rn(c.beta, wr));
+          wv[r] = pn;
+          rzb += rres * zr;
+          wr = pn;
+        }
+        const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, tt), dr), wr);
+        const double yb = __dadd_rn(tt, __dmul_rn(dr, wr));
+        E.y[op.n + r] = yb;
+        pacc += tt * z + wr * yb;
+        S.zs[g][rr] = z;
       }
-      consumer_bar();
+      tile_group_bar(g);
+      for (int cc = tid; cc < nd; cc += T) {
+        double s0 = 0.0, s1 = 0.0;
+        int rr = 0;
+        for (; rr + 1 < R; rr += 2) {
+          s0 = fma(st.a[rr * pitch + cc], S.zs[g][rr], s0);
+          s1 = fma(st.a[(rr + 1) * pitch + cc], S.zs[g][rr + 1], s1);
+        }
+        if (rr < R) s0 = fma(st.a[rr * pitch + cc], S.zs[g][rr], s0);
+        D.bpart[td.d0 + cc] = s0 + s1;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&S.empty[s]);
     }
   }
   __syncthreads();
-  pacc += hess_rows(op, v, E.y, E.part, E.G, S.red, S.s_lr);
+  // (the non-diagonal Hessian part runs in k_slot_hess: more blocks than this grid)
   double t = block_sum(pacc, S.red);
   if (threadIdx.x == 0) E.part[SLOT_ROWS * E.G + blockIdx.x] = t;
   t = block_sum(rzb, S.red);
   if (threadIdx.x == 0) E.part[SLOT_AUX2 * E.G + blockIdx.x] = t;
+}
+
+// y_top += H' u for CSR / dense / low-rank H, its u'H'u added to the slot's
+// PREP partial (same grid as the top kernel)
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
+  __shared__ double red[32];
+  __shared__ double s_lr[QPK_KMAX];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
+  const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
+  const double acc = hess_rows(E.op, v, E.y, E.part, E.G, red, s_lr);
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) E.part[SLOT_PREP * E.G + blockIdx.x] += t;
+}
+
+// out[j] (+)= sum of column j's tile partials (a warp per column, fixed order)
+__global__ void __launch_bounds__(QPK_BLOCK) k_tile_combine(Engine E, double* out, int add, int par) {
+  if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  for (int j = gwarp; j < E.op.n; j += nwarp) {
+    const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
+    double s0 = 0.0;
+    for (int q = qb + lane; q < qe; q += 32) s0 += E.dict.bpart[__ldg(E.dict.col_pos + q)];
+    s0 = subwarp_sum<32>(s0);
+    if (lane == 0) out[j] = add ? out[j] + s0 : s0;
+  }
+}
+
+// Jacobi through the tiles: bpart[c] = sum_r A[r][c]^2 / d_r (once per IPM iteration)
+__global__ void __launch_bounds__(QPK_BLOCK) k_jac_tile(Engine E) {
+  const Dict& D = E.dict;
+  for (int t = blockIdx.x; t < D.nblk; t += gridDim.x) {
+    const TileDescD td = D.tiles[t];
+    const int R = td.rb - td.ra;
+    for (int cc = threadIdx.x; cc < td.ndp; cc += blockDim.x) {
+      double s0 = 0.0;
+      for (int rr = 0; rr < R; ++rr) {
+        const double a = __ldg(D.tval + td.v0 + (size_t)rr * td.pad0 + cc);
+        s0 += __dmul_rn(a, a) * (1.0 / __ldg(E.op.d + td.ra + rr));
+      }
+      D.bpart[td.d0 + cc] = s0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
