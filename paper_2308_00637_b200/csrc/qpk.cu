@@ -493,7 +493,9 @@ struct qpk_ctx {
   DBuf<double> seg_sum;
   int n_seg = 0, seg_lanes = 8;
   // row-block dictionaries
-  DBuf<int> dcols, col_ptr, col_pos;
+  DBuf<int> dcols, col_ptr, col_pos, comb_beg, comb_col;
+  DBuf<double> comb_sum;
+  int comb_lanes = 8, comb_nseg = 0;
   DBuf<TileDescD> tiles;
   DBuf<double> tval;
   DBuf<int4> rtile_desc;
@@ -501,7 +503,7 @@ struct qpk_ctx {
   int tma_rows = -1;              // -1 auto (env QPK_TMA_ROWS)
   DBuf<double> bpart;
   int nblk = 0;
-  bool have_dict = false;
+  bool have_dict = false, h_tiled = false;
   double dict_reuse = 0.0;        // tile density: nonzeros / dense tile slots
   DBuf<double> bv, cv, hh, hv, hdense, U, w, hdiag;
   bool have_csc = false;
@@ -744,7 +746,11 @@ int qpk_set_hessian_csr(qpk_ctx* c, const int64_t* ro, const int64_t* ci, const 
     if (ci[k] < 0 || ci[k] >= c->n) return fail(QPK_E_ARG, "Hessian column out of range");
     c->h_hci[k] = (int)ci[k];
   }
-  c->h_lanes = pow2_clamp((nnz + c->n - 1) / std::max<long long>(c->n, 1), 1, 32);
+  // lanes per H row from the NON-EMPTY rows (RT Hessians: most beamlets never
+  // touch the target, the rest have hundreds of entries), ~5 entries per lane
+  long long nonempty = 0;
+  for (long long j = 0; j < c->n; ++j) nonempty += ro[j + 1] > ro[j];
+  c->h_lanes = pow2_clamp((nnz + std::max<long long>(nonempty, 1) - 1) / std::max<long long>(nonempty, 1) / 5, 1, 32);
   return QPK_OK;
 }
 
@@ -827,67 +833,99 @@ static int build_csc(qpk_ctx* c) {
 // sorted column list.  have_dict = false when a single row is too wide.
 static int build_dict(qpk_ctx* c) {
   c->have_dict = false;
+  c->h_tiled = false;
   const long long n = c->n, m = c->m;
   std::vector<int> mark(n, -1), cur;
   std::vector<TileDescD> tiles;
   std::vector<int> cols;
   std::vector<double> tval;
   cur.reserve(QPK_TILE_DMAX);
-  long long slots = 0;
-  long long r = 0;
   int tid = 0;
   auto r4 = [](long long x) { return (x + 3) & ~3LL; };
-  while (r < m) {
-    const long long ra = r;
-    cur.clear();
-    while (r < m) {
-      long long fresh = 0;
-      for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
-        const int col = c->h_ci[k];
-        if (col >= 0 && mark[col] != tid) ++fresh;
+  // tile the rows [0, nrows) of a CSR matrix; returns dense slots, or -1 if a
+  // row is wider than a tile
+  auto tile_rows = [&](const int* rp, const int* ci, const double* v, long long nrows, int kind) -> long long {
+    long long slots = 0, r = 0;
+    while (r < nrows) {
+      const long long ra = r;
+      cur.clear();
+      while (r < nrows) {
+        long long fresh = 0;
+        for (int k = rp[r]; k < rp[r + 1]; ++k)
+          if (ci[k] >= 0 && mark[ci[k]] != tid) ++fresh;
+        const long long nd = (long long)cur.size() + fresh, rows = r - ra + 1;
+        if (r4(nd) > QPK_TILE_DMAX || rows * (r4(nd) | 1) > QPK_TILE_DOUBLES || rows > QPK_TILE_ROWS) {
+          if (r == ra) return -1;
+          break;
+        }
+        for (int k = rp[r]; k < rp[r + 1]; ++k)
+          if (ci[k] >= 0 && mark[ci[k]] != tid) { mark[ci[k]] = tid; cur.push_back(ci[k]); }
+        ++r;
       }
-      const long long nd = (long long)cur.size() + fresh, rows = r - ra + 1;
-      if (r4(nd) > QPK_TILE_DMAX || rows * (r4(nd) | 1) > QPK_TILE_DOUBLES || rows > QPK_TILE_ROWS) {
-        if (r == ra) return QPK_OK;                    // one row alone does not fit a tile
-        break;
-      }
-      for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
-        const int col = c->h_ci[k];
-        if (col >= 0 && mark[col] != tid) { mark[col] = tid; cur.push_back(col); }
-      }
-      ++r;
+      std::sort(cur.begin(), cur.end());
+      const int ndp = (int)r4((long long)cur.size());
+      const int pitch = ndp | 1;                        // odd row pitch: conflict-free column reads
+      TileDescD td;
+      td.ra = (int)ra; td.rb = (int)r; td.d0 = (int)cols.size(); td.ndp = ndp;
+      td.v0 = (int)((tval.size() + 1) & ~(size_t)1);  // 16-byte aligned block start
+      td.pad0 = pitch; td.pad1 = kind; td.pad2 = 0;
+      if ((long long)td.v0 + (r - ra) * pitch >= (1LL << 31) - 64) return -1;
+      for (int col : cur) cols.push_back(col);
+      for (int i = (int)cur.size(); i < ndp; ++i) cols.push_back(-1);
+      const size_t base = td.v0;
+      tval.resize(base + (size_t)(r - ra) * pitch, 0.0);
+      for (long long rr = ra; rr < r; ++rr)
+        for (int k = rp[rr]; k < rp[rr + 1]; ++k) {
+          if (ci[k] < 0) continue;
+          const int pos = (int)(std::lower_bound(cur.begin(), cur.end(), ci[k]) - cur.begin());
+          tval[base + (size_t)(rr - ra) * pitch + pos] = v[k];
+        }
+      slots += (r - ra) * pitch;
+      tiles.push_back(td);
+      ++tid;
     }
-    std::sort(cur.begin(), cur.end());
-    const int ndp = (int)r4((long long)cur.size());
-    const int pitch = ndp | 1;                          // odd row pitch: conflict-free column reads
-    TileDescD td;
-    td.ra = (int)ra; td.rb = (int)r; td.d0 = (int)cols.size(); td.ndp = ndp;
-    td.v0 = (int)((tval.size() + 1) & ~(size_t)1);    // 16-byte aligned block start
-    td.pad0 = pitch; td.pad1 = td.pad2 = 0;
-    if ((long long)td.v0 + (r - ra) * pitch >= (1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "tiles exceed int32");
-    for (int col : cur) cols.push_back(col);
-    for (int i = (int)cur.size(); i < ndp; ++i) cols.push_back(-1);
-    const size_t base = td.v0;
-    tval.resize(base + (size_t)(r - ra) * pitch, 0.0);
-    for (long long rr = ra; rr < r; ++rr)
-      for (int k = c->h_rp[rr]; k < c->h_rp[rr + 1]; ++k) {
-        const int col = c->h_ci[k];
-        if (col < 0) continue;
-        const int pos = (int)(std::lower_bound(cur.begin(), cur.end(), col) - cur.begin());
-        tval[base + (size_t)(rr - ra) * pitch + pos] = c->h_v[k];
-      }
-    slots += (r - ra) * pitch;
-    tiles.push_back(td);
-    ++tid;
+    return slots;
+  };
+  const long long slots = tile_rows(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), m, 0);
+  if (slots < 0) return QPK_OK;
+  const size_t n_bcols = cols.size();
+  const int n_btiles = tid;
+  // the sparse Hessian's rows as dense tiles too (top-block rows, no B'z part),
+  // when they are dense enough -- the owner rank only
+  if (c->hkind == QPK_HESS_CSR && c->rank == 0 && !c->h_hci.empty()) {
+    const size_t t0 = tiles.size(), c0 = cols.size(), v0 = tval.size();
+    const long long hs = tile_rows(c->h_hrp.data(), c->h_hci.data(), c->h_hv.data(), n, 1);
+    if (hs > 0 && (double)c->h_hci.size() / (double)hs >= 0.5) {
+      c->h_tiled = true;
+    } else {
+      tiles.resize(t0); cols.resize(c0); tval.resize(v0); tid = n_btiles;
+    }
   }
-  // column -> its tile-partial positions, in tile order
+  // column -> its B-tile-partial positions, in tile order
   std::vector<int> col_ptr(n + 1, 0), col_pos;
-  for (int col : cols) if (col >= 0) col_ptr[col + 1]++;
+  for (size_t p = 0; p < n_bcols; ++p) if (cols[p] >= 0) col_ptr[cols[p] + 1]++;
   for (long long j = 0; j < n; ++j) col_ptr[j + 1] += col_ptr[j];
   col_pos.resize(col_ptr[n]);
   {
     std::vector<int> at(col_ptr.begin(), col_ptr.end() - 1);
-    for (size_t p = 0; p < cols.size(); ++p) if (cols[p] >= 0) col_pos[at[cols[p]]++] = (int)p;
+    for (size_t p = 0; p < n_bcols; ++p) if (cols[p] >= 0) col_pos[at[cols[p]]++] = (int)p;
+  }
+  {
+    // combine segments: each column's partial list in chunks of <= QPK_COMB_CHUNK
+    std::vector<int> cseg(n + 1, 0), cbeg;
+    for (long long j = 0; j < n; ++j) {
+      cseg[j] = (int)cbeg.size();
+      for (int b = col_ptr[j]; b < col_ptr[j + 1]; b += QPK_COMB_CHUNK) cbeg.push_back(b);
+    }
+    cseg[n] = (int)cbeg.size();
+    cbeg.push_back(col_ptr[n]);
+    c->comb_nseg = cseg[n];
+    const long long avg = (long long)col_pos.size() / std::max<long long>(c->comb_nseg, 1);
+    c->comb_lanes = pow2_clamp((avg + 3) / 4, 1, 32);
+    CUDA_TRY(upload(c->comb_col, cseg, c->stream));
+    CUDA_TRY(upload(c->comb_beg, cbeg, c->stream));
+    CUDA_TRY(c->comb_sum.alloc(std::max(c->comb_nseg, 1)));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
   cols.resize(cols.size() + 16, -1);                  // bulk copies read 16-byte windows
   tval.resize(tval.size() + 16, 0.0);
@@ -1063,7 +1101,8 @@ static int build_jacobi(qpk_ctx* c) {
     Engine E = make_engine(c);
     k_jac_tile<<<c->grid_eng, QPK_BLOCK, 0, s>>>(E);
     // column sums of the tile partials (sharded: summed over ranks), then the common finish
-    k_tile_combine<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 0, -1);
+    k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, -1);
+    k_comb_col<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 0, -1);
     int rc2 = allreduce_sum(c, c->y.p, c->n, s);
     if (rc2) return rc2;
     k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
@@ -1168,8 +1207,9 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   if (c->scatter == QPK_SCATTER_DICT) {
     k_slot_rows_tile<<<E.G_rows, (QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32,
                        sizeof(DTileSmem), s>>>(E, par);
-    k_tile_combine<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);   // y_top += B'z (tile partials)
-    if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, par);               // y_top += B'z (tile partials)
+    k_comb_col<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);
+    if (c->hkind != QPK_HESS_DIAG && !c->h_tiled) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
   } else {
     switch (c->lanes * 2 + (csc ? 1 : 0)) {
       case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
@@ -1222,6 +1262,9 @@ static Engine make_engine(qpk_ctx* c) {
   E.gscal = c->gscal.p; E.lscal2 = c->lscal2.p; E.abuf = c->abuf.p;
   E.dict.nblk = c->nblk; E.dict.tiles = c->tiles.p; E.dict.cols = c->dcols.p; E.dict.tval = c->tval.p;
   E.dict.bpart = c->bpart.p; E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
+  E.dict.comb_lanes = c->comb_lanes;
+  E.dict.nseg = c->comb_nseg; E.dict.seg_beg = c->comb_beg.p; E.dict.col_seg = c->comb_col.p;
+  E.dict.seg_sum = c->comb_sum.p;
   return E;
 }
 
@@ -1660,6 +1703,7 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "rank") return c->rank;
   if (k == "dict_blocks") return c->nblk;
   if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
+  if (k == "hess_tiled") return c->h_tiled ? 1 : 0;
   if (k == "block") return QPK_BLOCK;
   if (k == "sms") return c->sms;
   if (k == "hess_kind") return c->hkind;

@@ -63,6 +63,11 @@ struct Dict {
   double* bpart;
   const int* col_ptr;
   const int* col_pos;
+  int comb_lanes;            // lanes per combine segment
+  int nseg;                  // combine segments (<= QPK_COMB_CHUNK partials each)
+  const int* seg_beg;        // segment q: col_pos[seg_beg[q] .. seg_beg[q+1])
+  const int* col_seg;        // column j: segments [col_seg[j], col_seg[j+1])
+  double* seg_sum;
 };
 
 struct Engine {
@@ -289,24 +294,6 @@ __device__ __forceinline__ double top_value(const Engine& E, int j) {
   return E.y[j] + s;
 }
 
-// jac_top = (diag(H) + q) + 2 sum of the column's partials ; bottom = D
-__global__ void k_jac_dict_finish(Engine E, const double* hdiag, double* jac, double* minv) {
-  const Op& op = E.op;
-  const int N = op.n + op.m;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    double v;
-    if (i < op.n) {
-      double s = 0.0;
-      const int qb = __ldg(E.dict.col_ptr + i), qe = __ldg(E.dict.col_ptr + i + 1);
-      for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
-      v = __dadd_rn(__dadd_rn(__ldg(hdiag + i), __ldg(op.q + i)), __dmul_rn(2.0, s));
-    } else {
-      v = __ldg(op.d + (i - op.n));
-    }
-    jac[i] = v;
-    minv[i] = 1.0 / v;
-  }
-}
 
 // Sharded slot: finish this rank's top block (y_top + its local B'z
 // partials) and the rank-local totals of the slot's scalar partials, both
@@ -328,15 +315,6 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_shard_reduce(Engine E, int par) {
   if (threadIdx.x == 0) { E.gscal[0] = t0; E.gscal[1] = t1; E.gscal[2] = t2; E.gscal[3] = t3; }
 }
 
-// column sums of the dictionary block partials (Jacobi in sharded mode)
-__global__ void k_dict_col_sum(Engine E, double* out) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x) {
-    double s = 0.0;
-    const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
-    for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
-    out[j] = s;
-  }
-}
 
 // The PCG control decision after a slot (one thread): next mode, iteration
 // count, best iterate, beta -- linalg.py:104-133 for the scalars.

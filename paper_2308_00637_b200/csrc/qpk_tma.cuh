@@ -147,6 +147,12 @@ k_slot_rows_tile(Engine E, int par) {
         st.w0 = w0;
         const uint32_t b_a = round_up16((uint32_t)((td.rb - td.ra) * td.pad0) * 8u);
         const uint32_t b_c = round_up16((uint32_t)td.ndp * 4u);
+        if (td.pad1) {                                  // Hessian tile: no per-row vectors
+          mbar_expect_tx(&S.full[s], b_a + b_c);
+          bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
+          bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
+          continue;
+        }
         const uint32_t b_d = round_up16((uint32_t)(((td.rb + 1) & ~1) - v0) * 8u);
         const uint32_t b_w = round_up16((uint32_t)(((op.n + td.rb + 1) & ~1) - w0) * 8u);
         mbar_expect_tx(&S.full[s], b_a + b_c + b_d + b_w + (fuse ? 2 * b_w : 0u));
@@ -217,6 +223,21 @@ k_slot_rows_tile(Engine E, int par) {
         }
       }
       tile_group_bar(g);
+      if (td.pad1) {
+        // Hessian tile: rows are top indices j; y_j += (H u)_j, p'Hp partial
+        for (int rr = tid; rr < R; rr += T) {
+          double tt = 0.0;
+#pragma unroll
+          for (int ww = 0; ww < QPK_TILE_GWARPS; ++ww) tt += S.rpart[g][ww][rr];
+          const int j = td.ra + rr;
+          E.y[j] += tt;
+          pacc += v[j] * tt;
+        }
+        tile_group_bar(g);                              // rpart is rewritten by the next tile
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&S.empty[s]);
+        continue;
+      }
       for (int rr = tid; rr < R; rr += T) {
         double tt = 0.0;
 #pragma unroll
@@ -263,7 +284,9 @@ k_slot_rows_tile(Engine E, int par) {
 }
 
 // y_top += H' u for CSR / dense / low-rank H, its u'H'u added to the slot's
-// PREP partial (same grid as the top kernel)
+// PREP partial (same grid as the top kernel).  CSR H: LH lanes per row with
+// four independent gathers in flight per lane; y_j is final after the tile
+// combine, so the row owner adds without atomics.
 __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
   __shared__ double red[32];
   __shared__ double s_lr[QPK_KMAX];
@@ -271,22 +294,75 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
   if (c.mode == MODE_DONE) return;
   const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
   const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
-  const double acc = hess_rows(E.op, v, E.y, E.part, E.G, red, s_lr);
+  const Op& op = E.op;
+  double acc = 0.0;
+  if (op.H.kind == HESS_CSR && op.top_owner) {
+    const int LH = op.H.lanes, lh = threadIdx.x & (LH - 1);
+    const int per = 32 / LH, sw = (threadIdx.x & 31) / LH;
+    const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+    for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
+      const int j = (int)jb + sw;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      if (j < op.n) {
+        const int b = __ldg(op.H.rp + j), e = __ldg(op.H.rp + j + 1);
+        int k = b + lh;
+        for (; k + 3 * LH < e; k += 4 * LH) {
+          const int c0 = __ldg(op.H.ci + k), c1 = __ldg(op.H.ci + k + LH);
+          const int c2 = __ldg(op.H.ci + k + 2 * LH), c3 = __ldg(op.H.ci + k + 3 * LH);
+          s0 = fma(__ldg(op.H.v + k), v[c0], s0);
+          s1 = fma(__ldg(op.H.v + k + LH), v[c1], s1);
+          s2 = fma(__ldg(op.H.v + k + 2 * LH), v[c2], s2);
+          s3 = fma(__ldg(op.H.v + k + 3 * LH), v[c3], s3);
+        }
+        for (; k < e; k += LH) s0 = fma(__ldg(op.H.v + k), v[__ldg(op.H.ci + k)], s0);
+      }
+      double sum = (s0 + s1) + (s2 + s3);
+      for (int o = LH / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (j < op.n && lh == 0) { E.y[j] += sum; acc += v[j] * sum; }
+    }
+  } else {
+    acc = hess_rows(op, v, E.y, E.part, E.G, red, s_lr);
+  }
   const double t = block_sum(acc, red);
   if (threadIdx.x == 0) E.part[SLOT_PREP * E.G + blockIdx.x] += t;
 }
 
-// out[j] (+)= sum of column j's tile partials (a warp per column, fixed order)
-__global__ void __launch_bounds__(QPK_BLOCK) k_tile_combine(Engine E, double* out, int add, int par) {
+// Column sums of the B-tile partials in two deterministic levels, balanced for
+// columns present in thousands of tiles (cfg2's dense X block):
+//   k_comb_seg:  seg_sum[q] = sum of <= QPK_COMB_CHUNK partials of one column
+//                (LC lanes per segment, lane-strided then a butterfly)
+//   k_comb_col:  out[j] (+)= sum of column j's segment sums, in order
+#define QPK_COMB_CHUNK 128
+__global__ void __launch_bounds__(QPK_BLOCK) k_comb_seg(Engine E, int par) {
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
-  const int lane = threadIdx.x & 31;
+  const int LC = E.dict.comb_lanes, lc = threadIdx.x & (LC - 1);
+  const int per = 32 / LC, sw = (threadIdx.x & 31) / LC;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
-  for (int j = gwarp; j < E.op.n; j += nwarp) {
-    const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
-    double s0 = 0.0;
-    for (int q = qb + lane; q < qe; q += 32) s0 += E.dict.bpart[__ldg(E.dict.col_pos + q)];
-    s0 = subwarp_sum<32>(s0);
-    if (lane == 0) out[j] = add ? out[j] + s0 : s0;
+  for (long long qb = (long long)gwarp * per; qb < E.dict.nseg; qb += (long long)nwarp * per) {
+    const int q = (int)qb + sw;
+    double s0 = 0.0, s1 = 0.0;
+    if (q < E.dict.nseg) {
+      const int b = __ldg(E.dict.seg_beg + q), e = __ldg(E.dict.seg_beg + q + 1);
+      int k = b + lc;
+      for (; k + LC < e; k += 2 * LC) {
+        s0 += E.dict.bpart[__ldg(E.dict.col_pos + k)];
+        s1 += E.dict.bpart[__ldg(E.dict.col_pos + k + LC)];
+      }
+      if (k < e) s0 += E.dict.bpart[__ldg(E.dict.col_pos + k)];
+    }
+    double sum = s0 + s1;
+    for (int o = LC / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (q < E.dict.nseg && lc == 0) E.dict.seg_sum[q] = sum;
+  }
+}
+
+__global__ void __launch_bounds__(QPK_BLOCK) k_comb_col(Engine E, double* out, int add, int par) {
+  if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x) {
+    const int qb = __ldg(E.dict.col_seg + j), qe = __ldg(E.dict.col_seg + j + 1);
+    double sum = 0.0;
+    for (int q = qb; q < qe; ++q) sum += E.dict.seg_sum[q];
+    out[j] = add ? out[j] + sum : sum;
   }
 }
 
@@ -295,6 +371,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_jac_tile(Engine E) {
   const Dict& D = E.dict;
   for (int t = blockIdx.x; t < D.nblk; t += gridDim.x) {
     const TileDescD td = D.tiles[t];
+    if (td.pad1) continue;                              // Hessian tiles: diag(H) is precomputed
     const int R = td.rb - td.ra;
     for (int cc = threadIdx.x; cc < td.ndp; cc += blockDim.x) {
       double s0 = 0.0;
