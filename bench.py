@@ -325,14 +325,17 @@ def run_ours(args):
     achieved = per_launch / world / (avg_ms * 1e-3) / 1e9     # per GPU
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
-    prof = ROOT / "profiles" / "r01_pcg_kernel_dram.json"
+    traffic, traffic_src = None, None
+    prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+            rec = json.loads(prof.read_text()).get(args.workload)
+            if rec and args.scale == 1.0 and world == 1:
+                # ncu DRAM bytes of the same solve (per-iteration figure x iterations + final apply)
+                traffic = float(rec["dram_bytes_per_iter"]) * (args.iters + 1)
+                traffic_src = rec.get("source")
         except Exception:
             traffic = None
-
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -342,7 +345,7 @@ def run_ours(args):
             "config": {"workload": WORKLOAD_DESC[args.workload] + (f" (scale {args.scale})" if args.scale != 1 else "")
                                    + f"; {args.iters} PCG iterations per step (+ Jacobi build + final apply)",
                        "parallelism": f"rowshard{world} (NCCL all-reduce per iteration)" if world > 1 else "single",
-                       "scatter": {1: "atomic", 2: "csc", 3: "dict"}.get(gk.ctx.query("scatter"), "?"),
+                       "scatter": {1: "atomic", 2: "csc", 3: "dict", 4: "panel"}.get(gk.ctx.query("scatter"), "?"),
                        "l2": "inputs larger than L2" if per_iter > 126e6 else
                        "working set fits L2 (each step re-reads it every PCG iteration; no flush)",
                        "n": op.n, "m_B": op.m, "nnz_B": gk.ctx.query("nnz"),
@@ -351,7 +354,7 @@ def run_ours(args):
                                  "persistent cooperative kernel",
                        "seed": meta["seed"]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": per_launch, "algorithmic_bytes_per_iter": per_iter,
                          "kernel": ("slot engine kernels k_slot_top/rows/update (whole solve)" if engine_used else
                                     f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if gk.ctx.query('scatter') == 2 else 'false'}>"),

@@ -63,9 +63,13 @@ enum {
   QPK_SCATTER_ATOMIC = 1,  /* one pass over B, fp64 atomics (order not reproducible) */
   QPK_SCATTER_CSC = 2,     /* second, gather-only pass over a resident CSC copy:
                               bitwise reproducible run to run */
-  QPK_SCATTER_DICT = 3     /* one pass; rows grouped into blocks with a shared-memory
+  QPK_SCATTER_DICT = 3,    /* one pass; rows grouped into blocks with a shared-memory
                               column dictionary, per-block partials combined in a
                               fixed order: no atomics, bitwise reproducible */
+  QPK_SCATTER_PANEL = 4    /* one pass; columns present in most rows stored as a dense
+                              row-major panel (B'z partials in registers, combined
+                              per CTA in a fixed order), the rest of each row as a
+                              narrow ELL strip: bitwise reproducible */
 };
 
 typedef struct qpk_ctx qpk_ctx;

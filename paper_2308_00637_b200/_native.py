@@ -19,7 +19,7 @@ LIB_PATH = Path(os.environ.get("QPK_LIB", Path(__file__).resolve().parent / "lib
 QPK_OK = 0
 QPK_HESS_DIAG, QPK_HESS_CSR, QPK_HESS_DENSE, QPK_HESS_LOWRANK = 0, 1, 2, 3
 QPK_PCG_OK, QPK_PCG_BREAKDOWN = 0, 1
-QPK_SCATTER_AUTO, QPK_SCATTER_ATOMIC, QPK_SCATTER_CSC, QPK_SCATTER_DICT = 0, 1, 2, 3
+QPK_SCATTER_AUTO, QPK_SCATTER_ATOMIC, QPK_SCATTER_CSC, QPK_SCATTER_DICT, QPK_SCATTER_PANEL = 0, 1, 2, 3, 4
 
 EXPORTED = (
     "qpk_abi_version", "qpk_last_error", "qpk_create", "qpk_destroy", "qpk_set_stream",

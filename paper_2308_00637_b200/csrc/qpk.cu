@@ -27,6 +27,7 @@
 #include "qpk_device.cuh"
 #include "qpk_engine.cuh"
 #include "qpk_tma.cuh"
+#include "qpk_panel.cuh"
 #include "qpk_ipm.cuh"
 #include <chrono>
 
@@ -507,6 +508,11 @@ struct qpk_ctx {
   double dict_reuse = 0.0;        // tile density: nonzeros / dense tile slots
   DBuf<double> bv, cv, hh, hv, hdense, U, w, hdiag;
   bool have_csc = false;
+  // dense column panel (QPK_SCATTER_PANEL)
+  bool have_panel = false;
+  int panel_kp = 0, panel_q = 0, panel_ew = 0, panel_direct = 0, panel_grid = 0, panel_kd = 0;
+  DBuf<double> panel_P, panel_ev, panel_part, panel_ue, panel_yrem;
+  DBuf<int> panel_cols, panel_eci, panel_cpos;
 
   // per IPM iteration
   DBuf<double> d, q, jac, minv;
@@ -606,6 +612,48 @@ static void launch_jac_rows(int lanes, int grid, cudaStream_t s, const Op& o, do
     case 8: k_jac_rows<8><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
     case 16: k_jac_rows<16><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
     default: k_jac_rows<32><<<grid, QPK_BLOCK, 0, s>>>(o, acc); break;
+  }
+}
+
+static const int kPanelQ[] = {1, 2, 4, 6, 8, 12, 16};
+
+
+template <int Q>
+static void launch_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E, int par) {
+  k_slot_panel<Q><<<c->panel_grid, (QPK_PANEL_CW + 1) * 32, panel_smem_bytes(c->panel_kp, c->panel_ew), s>>>(E, par);
+}
+template <int Q>
+static void launch_jac_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E) {
+  k_jac_panel<Q><<<c->panel_grid, QPK_PANEL_CW * 32, (size_t)QPK_PANEL_CW * c->panel_kp * sizeof(double), s>>>(E);
+}
+template <int Q>
+static cudaError_t panel_attr_t(const qpk_ctx* c) {
+  cudaError_t e = cudaFuncSetAttribute(k_slot_panel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)panel_smem_bytes(c->panel_kp, c->panel_ew));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_jac_panel<Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(QPK_PANEL_CW * c->panel_kp * sizeof(double)));
+}
+#define QPK_PANEL_DISPATCH(FN, ...)                   \
+  switch (c->panel_q) {                               \
+    case 1: FN<1>(__VA_ARGS__); break;                \
+    case 2: FN<2>(__VA_ARGS__); break;                \
+    case 4: FN<4>(__VA_ARGS__); break;                \
+    case 6: FN<6>(__VA_ARGS__); break;                \
+    case 8: FN<8>(__VA_ARGS__); break;                \
+    case 12: FN<12>(__VA_ARGS__); break;              \
+    default: FN<16>(__VA_ARGS__); break;              \
+  }
+
+static cudaError_t panel_attr(const qpk_ctx* c) {
+  switch (c->panel_q) {
+    case 1: return panel_attr_t<1>(c);
+    case 2: return panel_attr_t<2>(c);
+    case 4: return panel_attr_t<4>(c);
+    case 6: return panel_attr_t<6>(c);
+    case 8: return panel_attr_t<8>(c);
+    case 12: return panel_attr_t<12>(c);
+    default: return panel_attr_t<16>(c);
   }
 }
 
@@ -774,10 +822,11 @@ int qpk_set_hessian_lowrank(qpk_ctx* c, const double* h0, int64_t k, const doubl
 
 // B' as CSC, every column padded to a multiple of 4 entries (row -1, value 0);
 // rows inside a column ascend (deterministic gather order)
-static int build_csc(qpk_ctx* c) {
+static int build_csc(qpk_ctx* c, const std::vector<int>& h_rp, const std::vector<int>& h_ci,
+                     const std::vector<double>& h_v) {
   const long long n = c->n;
   std::vector<long long> cnt(n, 0);
-  for (int col : c->h_ci) if (col >= 0) cnt[col]++;
+  for (int col : h_ci) if (col >= 0) cnt[col]++;
   std::vector<int> cp(n + 1, 0);
   long long tot = 0;
   for (long long j = 0; j < n; ++j) {
@@ -790,12 +839,12 @@ static int build_csc(qpk_ctx* c) {
   std::vector<double> cv(tot, 0.0);
   std::vector<int> pos(cp.begin(), cp.end() - 1);
   for (long long r = 0; r < c->m; ++r)
-    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
-      const int col = c->h_ci[k];
+    for (int k = h_rp[r]; k < h_rp[r + 1]; ++k) {
+      const int col = h_ci[k];
       if (col < 0) continue;
       const int at = pos[col]++;
       ri[at] = (int)r;
-      cv[at] = c->h_v[k];
+      cv[at] = h_v[k];
     }
   // column segments for the engine's B'z pass: LS lanes x 8 entries each
   {
@@ -943,6 +992,97 @@ static int build_dict(qpk_ctx* c) {
   return QPK_OK;
 }
 
+// Dense column panel: the columns present in at least half of the rows,
+// stored as a dense row-major m x kp block (kp = 64 Q); every row's other
+// entries as an ELL strip of width ew <= 32, plus their CSC (Jacobi, and B'z
+// when a remainder column has several entries).  Chosen when the panel holds
+// >= 70 % of the nonzeros (the SVM primal: [diag(y)X, y | I]).
+static int build_panel(qpk_ctx* c, bool force) {
+  c->have_panel = false;
+  const long long n = c->n, m = c->m;
+  if (m == 0 || n == 0) return QPK_OK;
+  std::vector<long long> cnt(n, 0);
+  for (int col : c->h_ci) if (col >= 0) cnt[col]++;
+  std::vector<int> pos(n, -1), pcols;
+  long long pnnz = 0;
+  for (long long j = 0; j < n; ++j)
+    if (cnt[j] > 0 && 2 * cnt[j] >= m) { pos[j] = (int)pcols.size(); pcols.push_back((int)j); pnnz += cnt[j]; }
+  const long long kd = (long long)pcols.size();
+  if (kd == 0 || (!force && (kd < 32 || 10 * pnnz < 7 * c->nnz))) return QPK_OK;
+  int Q = 0;
+  for (int q : kPanelQ) if (64LL * q >= kd) { Q = q; break; }
+  if (!Q) return QPK_OK;
+  const int kp = 64 * Q;
+  // remainder: row widths and per-column counts
+  int ew = 0;
+  std::vector<int> rcnt(n, 0);
+  for (long long r = 0; r < m; ++r) {
+    int w = 0;
+    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+      const int col = c->h_ci[k];
+      if (col >= 0 && pos[col] < 0) { ++w; ++rcnt[col]; }
+    }
+    ew = std::max(ew, w);
+  }
+  if (ew > 32 || panel_smem_bytes(kp, ew) > 220 * 1024) return QPK_OK;
+  size_t fr = 0, tot = 0;
+  CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+  if ((double)m * kp * 8.0 > 0.4 * (double)fr) return QPK_OK;
+  bool direct = true;
+  for (long long j = 0; j < n; ++j) if (rcnt[j] > 1) { direct = false; break; }
+  const int ewa = std::max(ew, 1);
+  std::vector<double> P((size_t)m * kp, 0.0), ev((size_t)m * ewa, 0.0);
+  std::vector<int> eci((size_t)m * ewa, -1);
+  std::vector<int> rrp(m + 1, 0), rci;
+  std::vector<double> rv;
+  for (long long r = 0; r < m; ++r) {
+    int w = 0;
+    for (int k = c->h_rp[r]; k < c->h_rp[r + 1]; ++k) {
+      const int col = c->h_ci[k];
+      if (col < 0) continue;
+      if (pos[col] >= 0) {
+        P[(size_t)r * kp + pos[col]] = c->h_v[k];
+      } else {
+        eci[(size_t)r * ewa + w] = col;
+        ev[(size_t)r * ewa + w] = c->h_v[k];
+        ++w;
+        rci.push_back(col);
+        rv.push_back(c->h_v[k]);
+      }
+    }
+    rrp[r + 1] = (int)rci.size();
+  }
+  pcols.resize(kp, -1);
+  ev.resize(ev.size() + 8, 0.0);                  // bulk copies read 16-byte windows
+  eci.resize(eci.size() + 8, -1);
+  std::vector<int> cpos;
+  if (direct) {
+    cpos.assign(n, -1);
+    for (size_t p = 0; p < (size_t)m * ewa; ++p) if (eci[p] >= 0) cpos[eci[p]] = (int)p;
+  }
+  cudaStream_t s = c->stream;
+  if (direct && ew > 0) {
+    CUDA_TRY(upload(c->panel_cpos, cpos, s));
+    CUDA_TRY(c->panel_ue.alloc((size_t)m * ewa + 8));
+    CUDA_TRY(c->panel_yrem.alloc((size_t)m * ewa + 8));
+    CUDA_TRY(cudaMemsetAsync(c->panel_ue.p, 0, ((size_t)m * ewa + 8) * sizeof(double), s));
+  }
+  CUDA_TRY(upload(c->panel_P, P, s));
+  CUDA_TRY(upload(c->panel_cols, pcols, s));
+  CUDA_TRY(upload(c->panel_eci, eci, s));
+  CUDA_TRY(upload(c->panel_ev, ev, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  int rc = build_csc(c, rrp, rci, rv);        // the remainder's CSC (Jacobi; B'z when not direct)
+  if (rc) return rc;
+  c->panel_kp = kp;
+  c->panel_q = Q;
+  c->panel_ew = ew;
+  c->panel_kd = (int)kd;
+  c->panel_direct = direct ? 1 : 0;
+  c->have_panel = true;
+  return QPK_OK;
+}
+
 int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_finalize: no problem being built");
   const long long mB = c->m_e + c->m_l + c->m_u;
@@ -1011,7 +1151,16 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   // deterministic; DICT falls back to CSC when a row is wider than a dictionary.
   if (const char* ev = getenv("QPK_SCATTER")) if (scatter == QPK_SCATTER_AUTO) scatter = atoi(ev);
   c->scatter = QPK_SCATTER_ATOMIC;
-  if ((scatter == QPK_SCATTER_AUTO || scatter == QPK_SCATTER_DICT) && c->m > 0) {
+  // a dense column panel (large systems in AUTO) comes first
+  if (c->m > 0 && (scatter == QPK_SCATTER_PANEL || (scatter == QPK_SCATTER_AUTO && c->N() >= 50000))) {
+    int rc = build_panel(c, scatter == QPK_SCATTER_PANEL);
+    if (rc) return rc;
+    if (c->have_panel) scatter = QPK_SCATTER_PANEL;
+    else if (scatter == QPK_SCATTER_PANEL) scatter = QPK_SCATTER_CSC;     // no panel structure
+  }
+  if (scatter == QPK_SCATTER_PANEL) {
+    c->scatter = QPK_SCATTER_PANEL;
+  } else if ((scatter == QPK_SCATTER_AUTO || scatter == QPK_SCATTER_DICT) && c->m > 0) {
     int rc = build_dict(c);
     if (rc) return rc;
     // Dense tiles pay off when they are mostly nonzeros (banded / clustered
@@ -1025,7 +1174,7 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
       scatter = QPK_SCATTER_CSC;
   }
   if (scatter == QPK_SCATTER_CSC && c->m > 0) {
-    int rc = build_csc(c);
+    int rc = build_csc(c, c->h_rp, c->h_ci, c->h_v);
     if (rc) return rc;
     c->scatter = QPK_SCATTER_CSC;
   }
@@ -1043,6 +1192,10 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     int eng_per_sm = c->scatter == QPK_SCATTER_DICT ? 3 : 4;
     const long long ework = std::max<long long>((long long)c->h_ci.size() / 512, N / 256);
     c->grid_eng = (int)std::max<long long>(1, std::min<long long>((long long)eng_per_sm * c->sms, ework));
+  }
+  if (c->scatter == QPK_SCATTER_PANEL) {
+    c->panel_grid = std::max(1, std::min(c->sms, c->grid_eng));      // one CTA per SM
+    CUDA_TRY(c->panel_part.alloc((size_t)c->panel_grid * c->panel_kp));
   }
   CUDA_TRY(c->part.alloc((size_t)NSLOTS * std::max(c->grid_pcg, c->grid_eng)));
   if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
@@ -1095,6 +1248,23 @@ static int build_jacobi(qpk_ctx* c) {
   Op o = c->op();
   const int G = c->grid_std;
   cudaStream_t s = c->stream;
+  if (c->scatter == QPK_SCATTER_PANEL) {
+    // remainder columns through their CSC (writes every column, 0 for the
+    // panel's), then the panel columns from the per-CTA partials
+    int rc = engine_setup(c);
+    if (rc) return rc;
+    Engine E = make_engine(c);
+    k_jac_cols<<<G, QPK_BLOCK, 0, s>>>(o, c->y.p);
+    QPK_PANEL_DISPATCH(launch_jac_panel_t, c, s, E);
+    k_panel_comb<<<c->panel_kp / 32, 256, 0, s>>>(E, c->y.p, 1, -1);     // panel columns only
+    int rc2 = allreduce_sum(c, c->y.p, c->n, s);
+    if (rc2) return rc2;
+    k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
+    c->launches += 4;
+    CUDA_TRY(cudaGetLastError());
+    c->jac_ready = true;
+    return QPK_OK;
+  }
   if (c->scatter == QPK_SCATTER_DICT) {
     int rc = engine_setup(c);
     if (rc) return rc;
@@ -1140,7 +1310,10 @@ int qpk_jacobi(qpk_ctx* c, double* diag_out) {
   return QPK_OK;
 }
 
+static int apply_engine(qpk_ctx* c, const double* v_dev, double* y_dev);
+
 static int apply_impl(qpk_ctx* c, const double* v_dev, double* y_dev) {
+  if (c->scatter == QPK_SCATTER_DICT || c->scatter == QPK_SCATTER_PANEL) return apply_engine(c, v_dev, y_dev);
   Op o = c->op();
   const int G = c->grid_std;
   cudaStream_t s = c->stream;
@@ -1200,11 +1373,35 @@ static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const
   k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
 }
 
-static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
-  const bool csc = c->scatter == QPK_SCATTER_CSC;
+// does the slot finish B'z with a CSC gather pass (k_slot_csc + seg sums)?
+static bool slot_csc(const qpk_ctx* c) {
+  return c->scatter == QPK_SCATTER_CSC || (c->scatter == QPK_SCATTER_PANEL && !c->panel_direct);
+}
+
+static int slot_launches(const qpk_ctx* c) {
+  int k = 2;                                                    // top, update
+  if (c->scatter == QPK_SCATTER_DICT) k += 3 + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
+  else if (c->scatter == QPK_SCATTER_PANEL) k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0);
+  else k += 1 + (slot_csc(c) ? 1 : 0);
+  if (c->sharded) k += 2;
+  return k;
+}
+
+// the operator part of a slot: top, the pass over B (+ its B'z completion
+// into y_top, except the CSC segment sums, which the consumer adds)
+static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
+  const bool csc = slot_csc(c);
   const int G = c->grid_eng;
   k_slot_top<<<G, QPK_BLOCK, 0, s>>>(E, par);
-  if (c->scatter == QPK_SCATTER_DICT) {
+  if (c->scatter == QPK_SCATTER_PANEL) {
+    QPK_PANEL_DISPATCH(launch_panel_t, c, s, E, par);
+    // y_P += B'z (CTA partials); direct remainder: y[col] += yrem
+    const int rem_blocks = (c->panel_direct && c->panel_ew > 0)
+                               ? (int)std::min<long long>(2 * c->sms, (c->m * c->panel_ew + 255) / 256) : 0;
+    k_panel_comb<<<c->panel_kp / 32 + rem_blocks, 256, 0, s>>>(E, c->y.p, 1, par);
+    if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
+  } else if (c->scatter == QPK_SCATTER_DICT) {
     k_slot_rows_tile<<<E.G_rows, (QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32,
                        sizeof(DTileSmem), s>>>(E, par);
     k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, par);               // y_top += B'z (tile partials)
@@ -1227,6 +1424,12 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
     }
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   }
+}
+
+static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
+  const bool csc = slot_csc(c);
+  const int G = c->grid_eng;
+  launch_slot_apply(c, E, par, s);
   if (!c->sharded) {
     if (csc) k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
     else k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
@@ -1246,6 +1449,27 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   k_slot_decide<<<1, 32, 0, s>>>(E, par);
 }
 
+// K v through the same kernels a PCG slot runs (tile / panel modes): v goes
+// to x[0] and the slot runs as the explicit-residual apply (MODE_CHECK) of it
+static int apply_engine(qpk_ctx* c, const double* v_dev, double* y_dev) {
+  int rc = engine_setup(c);
+  if (rc) return rc;
+  cudaStream_t s = c->stream;
+  Ctrl h;
+  memset(&h, 0, sizeof h);
+  h.mode = MODE_CHECK;
+  CUDA_TRY(cudaMemcpyAsync(c->x[0].p, v_dev, c->N() * sizeof(double), cudaMemcpyDeviceToDevice, s));
+  CUDA_TRY(cudaMemcpyAsync(c->ctrl.p, &h, sizeof h, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));          // h is a stack object
+  Engine E = make_engine(c);
+  launch_slot_apply(c, E, 0, s);
+  if (slot_csc(c)) k_apply_finish<2><<<c->grid_eng, QPK_BLOCK, 0, s>>>(E, y_dev);
+  else k_apply_finish<1><<<c->grid_eng, QPK_BLOCK, 0, s>>>(E, y_dev);
+  c->launches += slot_launches(c) - 1;
+  CUDA_TRY(cudaGetLastError());
+  return allreduce_sum(c, y_dev, c->n, s);
+}
+
 static Engine make_engine(qpk_ctx* c) {
   Engine E;
   E.op = c->op();
@@ -1254,6 +1478,13 @@ static Engine make_engine(qpk_ctx* c) {
   E.r = c->r.p; E.p = c->p.p; E.y = c->y.p; E.zb = c->zb.p; E.minv = c->minv.p;
   E.part = c->part.p; E.G = c->grid_eng;
   E.G_rows = (c->scatter == QPK_SCATTER_DICT || use_tma_rows(c)) ? std::min(c->sms, c->grid_eng) : c->grid_eng;
+  if (c->scatter == QPK_SCATTER_PANEL) E.G_rows = c->panel_grid;
+  E.panel.kp = c->panel_kp; E.panel.ew = c->panel_ew; E.panel.direct = c->panel_direct; E.panel.G = c->panel_grid;
+  E.panel.P = c->panel_P.p; E.panel.pcols = c->panel_cols.p; E.panel.eci = c->panel_eci.p; E.panel.ev = c->panel_ev.p;
+  E.panel.ppart = c->panel_part.p;
+  const bool pdir = c->scatter == QPK_SCATTER_PANEL && c->panel_direct && c->panel_ew > 0;
+  E.panel.cpos = pdir ? c->panel_cpos.p : nullptr;
+  E.panel.ue = c->panel_ue.p; E.panel.yrem = c->panel_yrem.p;
   E.ctrl = c->ctrl.p; E.counter = c->counter.p; E.cfg = c->ecfg.p;
   E.seg_ptr = c->seg_ptr.p; E.seg_beg = c->seg_beg.p; E.seg_sum = c->seg_sum.p;
   E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
@@ -1272,6 +1503,7 @@ static int engine_setup(qpk_ctx* c) {
   if (c->ctrl.p) return QPK_OK;
   CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sizeof(DTileSmem)));
+  if (c->scatter == QPK_SCATTER_PANEL) CUDA_TRY(panel_attr(c));
   CUDA_TRY(c->ctrl.alloc(2));
   CUDA_TRY(c->gscal.alloc(4));
   CUDA_TRY(c->lscal2.alloc(2));
@@ -1332,7 +1564,7 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
     } else {
       for (int k = 0; k < CH; ++k) launch_slot(c, E, k & 1, s);
     }
-    c->launches += (3 + (c->scatter == QPK_SCATTER_CSC ? 1 : 0) + (c->sharded ? 2 : 0)) * CH;
+    c->launches += (long long)slot_launches(c) * CH;
     slots += CH;
     const int b = chunk & 1;
     CUDA_TRY(cudaMemcpyAsync(&c->pinned_mode[b], &c->ctrl.p[0].mode, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1359,7 +1591,8 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
 extern "C" {
 
 static bool use_engine(qpk_ctx* c) {
-  if (c->scatter == QPK_SCATTER_DICT || c->sharded) return true;   // dictionary kernels / collectives: engine only
+  if (c->scatter == QPK_SCATTER_DICT || c->scatter == QPK_SCATTER_PANEL || c->sharded)
+    return true;                                 // tile / panel kernels, collectives: engine only
   if (c->engine >= 0) return c->engine == 1;
   const char* env = getenv("QPK_ENGINE");
   if (env) return atoi(env) == 1;
@@ -1704,6 +1937,11 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "dict_blocks") return c->nblk;
   if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "hess_tiled") return c->h_tiled ? 1 : 0;
+  if (k == "panel_kp") return c->panel_kp;
+  if (k == "panel_cols") return c->panel_kd;
+  if (k == "panel_ew") return c->panel_ew;
+  if (k == "panel_direct") return c->panel_direct;
+  if (k == "panel_grid") return c->panel_grid;
   if (k == "block") return QPK_BLOCK;
   if (k == "sms") return c->sms;
   if (k == "hess_kind") return c->hkind;
@@ -1713,7 +1951,8 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
                c->hh.bytes() + c->hrp.bytes() + c->hci.bytes() + c->hv.bytes() + c->hdense.bytes() + c->U.bytes() +
                c->w.bytes() + c->hdiag.bytes() + c->d.bytes() + c->q.bytes() + c->jac.bytes() + c->minv.bytes() +
                c->r.bytes() + c->p.bytes() + c->y.bytes() + c->zb.bytes() + c->rhs.bytes() + c->part.bytes() +
-               c->vin.bytes() + c->hist.bytes();
+               c->vin.bytes() + c->hist.bytes() + c->panel_P.bytes() + c->panel_ev.bytes() + c->panel_eci.bytes() +
+               c->panel_part.bytes() + c->tval.bytes() + c->bpart.bytes();
     for (auto& x : c->x) b += x.bytes();
     return (int64_t)b;
   }

@@ -70,10 +70,35 @@ struct Dict {
   double* seg_sum;
 };
 
+// Dense column panel (the "panel" mode, for B with a block of dense columns --
+// the SVM primal's [diag(y)X, y | I]): the columns present in most rows are
+// stored as a dense row-major m x kp panel (no indices, 8 B per entry), the
+// rest of each row ("remainder", <= 32 entries) as a fixed-width ELL strip.
+// B'z of the panel accumulates in registers per warp, then per CTA
+// (ppart[cta][j]), combined over CTAs in a fixed order (k_panel_comb).
+struct Panel {
+  int kp;                     // padded panel width (multiple of 64)
+  int ew;                     // remainder ELL width (0..32)
+  int direct;                 // every remainder column has <= 1 entry: y[col] += z a written directly
+  int G;                      // CTAs of the panel kernel (partials)
+  const double* P;            // m x kp row-major
+  const int* pcols;           // kp panel columns (-1 pads)
+  const int* eci;             // m x ew remainder columns (-1 pads)
+  const double* ev;           // m x ew remainder values
+  double* ppart;              // G x kp per-CTA partials of B'z (or of sum B^2/d)
+  // direct mode: the remainder's u values are staged by the top kernel into
+  // ue[] (entry order), and its B'z terms leave the panel kernel in yrem[]
+  // (entry order), added to y by k_panel_comb -- no random access in the pass
+  const int* cpos;            // n: entry position of column j's remainder entry, or -1 (direct mode)
+  double* ue;                 // m x ew
+  double* yrem;               // m x ew
+};
+
 struct Engine {
   Op op;
   Dict dict;
-  int scatter;                // 1 atomic, 2 CSC segments, 3 row-block dictionary
+  Panel panel;
+  int scatter;                // 1 atomic, 2 CSC segments, 3 row-block dictionary, 4 dense panel
   int sharded;                // row-sharded over ranks: collectives between the slot kernels
   double* gscal;              // [4] rank-summed ROWS, PREP, AUX, AUX2 totals (sharded)
   double* lscal2;             // [2] r'r, r'z (rank-local, then rank-summed)
@@ -187,6 +212,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
       if (op.top_owner) rz += rj * zj;
       const double pn = restart ? zj : __dadd_rn(zj, __dmul_rn(c.beta, pold));
       E.p[j] = pn;
+      if (E.panel.cpos) { const int pp = __ldg(E.panel.cpos + j); if (pp >= 0) E.panel.ue[pp] = pn; }
       acc += prep_elem(op, j, pn, E.y);
       if (lr) lowrank_accum(op, j, pn, sacc);
     }
@@ -202,6 +228,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
       if (c.xupd) { xv = __dadd_rn(xs[i], __dmul_rn(c.alpha_prev, E.p[i])); xd[i] = xv; }
       if (i < op.n) {
         const double v = (c.xupd && target == c.xn) ? xv : xt[i];
+        if (E.panel.cpos) { const int pp = __ldg(E.panel.cpos + i); if (pp >= 0) E.panel.ue[pp] = v; }
         acc += prep_elem(op, i, v, E.y);
         if (lr) lowrank_accum(op, i, v, sacc);
       }
@@ -480,6 +507,15 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
     return;
   }
   decide(E, c, par, rr_tot, rz_tot, alpha, rz, t_upd);
+}
+
+// out = K v after the operator part of a MODE_CHECK slot (qpk_apply in the
+// tile / panel modes): y plus, in CSC mode, the top entries' segment sums
+template <int SC>
+__global__ void __launch_bounds__(QPK_BLOCK) k_apply_finish(Engine E, double* out) {
+  const int N = E.op.n + E.op.m;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+    out[i] = (SC != 1 && i < E.op.n) ? top_value<SC>(E, i) : E.y[i];
 }
 
 // decision after a sharded slot: the collective has summed rr / rz over ranks

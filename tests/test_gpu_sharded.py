@@ -38,7 +38,8 @@ def group():
     yield None
 
 
-@pytest.mark.parametrize("mode", [_native.QPK_SCATTER_ATOMIC, _native.QPK_SCATTER_CSC, _native.QPK_SCATTER_DICT])
+@pytest.mark.parametrize("mode", [_native.QPK_SCATTER_ATOMIC, _native.QPK_SCATTER_CSC, _native.QPK_SCATTER_DICT,
+                                  _native.QPK_SCATTER_PANEL])
 @pytest.mark.parametrize("name", sorted(SPECS))
 def test_sharded_world1_parity(group, name, mode):
     fn, kw = SPECS[name]
