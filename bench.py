@@ -359,7 +359,8 @@ def run_ours(args):
                          "kernel": ("slot engine kernels k_slot_top/rows/update (whole solve)" if engine_used else
                                     f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if gk.ctx.query('scatter') == 2 else 'false'}>"),
                          "kernel_ms_avg": avg_ms,
-                         "phase_us_per_iter": dict(zip(["direction_top", "rows_B_Bt", "residual_update", "other"],
+                         "phase_us_per_iter": dict(zip(["direction_top", "rows_B_Bt", "residual_update",
+                                                        "combine_Bt_partials" if engine_used else "other"],
                                                        [round(v * 1e3 / args.iters, 2) for v in np.mean(phase_ms, axis=0)])),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

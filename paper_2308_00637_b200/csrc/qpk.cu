@@ -620,7 +620,7 @@ static const int kPanelQ[] = {1, 2, 4, 6, 8, 12, 16};
 
 template <int Q>
 static void launch_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E, int par) {
-  k_slot_panel<Q><<<c->panel_grid, (QPK_PANEL_CW + 1) * 32, panel_smem_bytes(c->panel_kp, c->panel_ew), s>>>(E, par);
+  k_slot_panel<Q><<<c->panel_grid, QPK_PANEL_CW * 32, panel_smem_bytes(c->panel_kp, c->panel_ew), s>>>(E, par);
 }
 template <int Q>
 static void launch_jac_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E) {
@@ -1190,7 +1190,11 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   c->grid_std = c->grid_pcg;
   {
     int eng_per_sm = c->scatter == QPK_SCATTER_DICT ? 3 : 4;
-    const long long ework = std::max<long long>((long long)c->h_ci.size() / 512, N / 256);
+    long long ework = std::max<long long>((long long)c->h_ci.size() / 512, N / 256);
+    // panel mode: the engine grid only runs the vector kernels (top, update),
+    // which are latency-bound -- fewer, fuller blocks
+    if (c->scatter == QPK_SCATTER_PANEL) ework = std::max<long long>(2 * c->sms, N / 1024);
+    if (const char* ev = getenv("QPK_ENGINE_GRID")) ework = atoi(ev);
     c->grid_eng = (int)std::max<long long>(1, std::min<long long>((long long)eng_per_sm * c->sms, ework));
   }
   if (c->scatter == QPK_SCATTER_PANEL) {
@@ -1256,7 +1260,7 @@ static int build_jacobi(qpk_ctx* c) {
     Engine E = make_engine(c);
     k_jac_cols<<<G, QPK_BLOCK, 0, s>>>(o, c->y.p);
     QPK_PANEL_DISPATCH(launch_jac_panel_t, c, s, E);
-    k_panel_comb<<<c->panel_kp / 32, 256, 0, s>>>(E, c->y.p, 1, -1);     // panel columns only
+    k_panel_comb<<<c->panel_kp / 32, 1024, 0, s>>>(E, c->y.p, 1, -1);     // panel columns only
     int rc2 = allreduce_sum(c, c->y.p, c->n, s);
     if (rc2) return rc2;
     k_jac_finish<<<G, QPK_BLOCK, 0, s>>>(o, c->hdiag.p, c->y.p, c->jac.p, c->minv.p);
@@ -1397,8 +1401,8 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
     QPK_PANEL_DISPATCH(launch_panel_t, c, s, E, par);
     // y_P += B'z (CTA partials); direct remainder: y[col] += yrem
     const int rem_blocks = (c->panel_direct && c->panel_ew > 0)
-                               ? (int)std::min<long long>(2 * c->sms, (c->m * c->panel_ew + 255) / 256) : 0;
-    k_panel_comb<<<c->panel_kp / 32 + rem_blocks, 256, 0, s>>>(E, c->y.p, 1, par);
+                               ? (int)std::min<long long>(2 * c->sms, (c->m * c->panel_ew + 1023) / 1024) : 0;
+    k_panel_comb<<<c->panel_kp / 32 + rem_blocks, 1024, 0, s>>>(E, c->y.p, 1, par);
     if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   } else if (c->scatter == QPK_SCATTER_DICT) {
@@ -1482,6 +1486,7 @@ static Engine make_engine(qpk_ctx* c) {
   E.panel.kp = c->panel_kp; E.panel.ew = c->panel_ew; E.panel.direct = c->panel_direct; E.panel.G = c->panel_grid;
   E.panel.P = c->panel_P.p; E.panel.pcols = c->panel_cols.p; E.panel.eci = c->panel_eci.p; E.panel.ev = c->panel_ev.p;
   E.panel.ppart = c->panel_part.p;
+  E.panel.probe = getenv("QPK_PANEL_PROBE") ? atoi(getenv("QPK_PANEL_PROBE")) : 0;
   const bool pdir = c->scatter == QPK_SCATTER_PANEL && c->panel_direct && c->panel_ew > 0;
   E.panel.cpos = pdir ? c->panel_cpos.p : nullptr;
   E.panel.ue = c->panel_ue.p; E.panel.yrem = c->panel_yrem.p;
@@ -1584,7 +1589,7 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
   out->iterations = fin.k; out->converged = fin.converged; out->status = fin.status;
   out->restarts = fin.restarts; out->applies = fin.applies; out->result_buf = fin.result;
   out->final_norm = fin.final_norm; out->threshold = fin.thr; out->rhs_norm = fin.rhs_norm;
-  out->phase_ns[0] = fin.ph[0]; out->phase_ns[1] = fin.ph[1]; out->phase_ns[2] = fin.ph[2]; out->phase_ns[3] = 0;
+  out->phase_ns[0] = fin.ph[0]; out->phase_ns[1] = fin.ph[1]; out->phase_ns[2] = fin.ph[2]; out->phase_ns[3] = fin.ph[3];
   return QPK_OK;
 }
 

@@ -28,7 +28,7 @@ enum { MODE_NORMAL = 0, MODE_RESTART = 1, MODE_CHECK = 2, MODE_FINAL = 3, MODE_D
 struct Ctrl {
   int mode, k, cur, best, xn, xupd, status, converged, restarts, applies, result, pad;
   double rz, rnorm, best_rnorm, thr, rhs_norm, alpha_prev, beta, final_norm;
-  unsigned long long t_top, t_rows, t_upd, ph[4];
+  unsigned long long t_top, t_rows, t_upd, t_mid, ph[4];   // t_mid: start of the B'z combine (tile / panel)
 };
 
 struct EngineCfg {
@@ -81,6 +81,7 @@ struct Panel {
   int ew;                     // remainder ELL width (0..32)
   int direct;                 // every remainder column has <= 1 entry: y[col] += z a written directly
   int G;                      // CTAs of the panel kernel (partials)
+  int probe;                  // diagnostics only (env QPK_PANEL_PROBE): 1 = consumers skip the math
   const double* P;            // m x kp row-major
   const int* pcols;           // kp panel columns (-1 pads)
   const int* eci;             // m x ew remainder columns (-1 pads)
@@ -352,8 +353,14 @@ __device__ __forceinline__ void decide(const Engine& E, const Ctrl& c, int par, 
   Ctrl o = c;
   o.applies += 1;
   o.ph[0] += c.t_rows - c.t_top;
-  o.ph[1] += t_upd - c.t_rows;
+  if (c.t_mid > c.t_rows && c.t_mid < t_upd) {
+    o.ph[1] += c.t_mid - c.t_rows;
+    o.ph[3] += t_upd - c.t_mid;
+  } else {
+    o.ph[1] += t_upd - c.t_rows;
+  }
   o.ph[2] += now - t_upd;
+  o.t_mid = 0;
   const double nrm = sqrt(rr_tot);
   if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
     const int cur = c.xupd ? c.xn : c.cur;               // x_{k-1} was materialised this slot

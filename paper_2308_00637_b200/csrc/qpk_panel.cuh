@@ -43,12 +43,19 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+#ifndef QPK_PANEL_STAGES
 #define QPK_PANEL_STAGES 3        // ring stages (chunks in flight: up to S)
-#define QPK_PANEL_CW 8            // consumer warps per CTA (one CTA per SM, + 1 producer warp)
+#endif
+#define QPK_PANEL_CW 8            // warps per CTA, one CTA per SM (lane 0 of warp 0 also produces)
+#ifndef QPK_PANEL_CHUNK
 #define QPK_PANEL_CHUNK 65536     // target panel bytes per chunk (one bulk copy)
+#endif
+#ifndef QPK_PANEL_RPW
+#define QPK_PANEL_RPW 2           // rows per warp step (interleaved reduction chains), kp <= 512
+#endif
 
-template <int Q> struct PanelRpw { static constexpr int value = Q <= 8 ? 2 : 1; };  // rows per warp step
-__host__ __device__ __forceinline__ int panel_rpw(int kp) { return kp <= 512 ? 2 : 1; }
+template <int Q> struct PanelRpw { static constexpr int value = Q <= 8 ? QPK_PANEL_RPW : 1; };
+__host__ __device__ __forceinline__ int panel_rpw(int kp) { return kp <= 512 ? QPK_PANEL_RPW : 1; }
 
 // Shared-memory layout of one ring stage (a chunk of rc consecutive rows):
 // panel rows, the 4 bottom vectors' slices (d, w, r, x; 16-byte aligned
@@ -84,7 +91,8 @@ __host__ __device__ __forceinline__ size_t panel_smem_bytes(int kp, int ew) {
 
 // One pass over the panel + remainder (a PCG iteration's apply, or the
 // CHECK / FINAL apply of an iterate).  CTA b owns rows [m b / G, m (b+1) / G),
-// cut into chunks of rc consecutive rows.  A producer lane streams each chunk
+// cut into chunks of rc consecutive rows.  A producer lane (lane 0 of warp 0,
+// S - 1 chunks ahead of its own consumption) streams each chunk
 // -- its panel rows (one bulk copy), the slices of d, w, r, x the fused update
 // needs, its remainder entries and (direct mode) their u values staged by the
 // top kernel -- with cp.async.bulk into an S-stage ring (mbarrier
@@ -93,7 +101,7 @@ __host__ __device__ __forceinline__ size_t panel_smem_bytes(int kp, int ew) {
 // overlap; fixed order -> deterministic.  No random access in direct mode (the
 // remainder's B'z terms go to yrem in entry order).
 template <int Q>
-__global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engine E, int par) {
+__global__ void __launch_bounds__(QPK_PANEL_CW * 32, 1) k_slot_panel(Engine E, int par) {
   extern __shared__ __align__(128) double psm[];
   constexpr int S = QPK_PANEL_STAGES, CW = QPK_PANEL_CW, RPW = PanelRpw<Q>::value;
   const Ctrl c = E.ctrl[par];
@@ -106,7 +114,6 @@ __global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engin
   const int kp = P.kp, ew = P.ew, n = op.n;
   const bool direct = P.direct;
   const PanelStage L = panel_stage(kp, ew);
-  double* us = psm;                              // u_P  [kp]
   double* red = psm + kp;                        // [32]
   double* ring = psm + kp + 32;                  // [S][L.size]; reused as warp partials [CW][kp]
   unsigned long long* full = reinterpret_cast<unsigned long long*>(ring + (size_t)S * L.size);
@@ -116,11 +123,7 @@ __global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engin
     for (int k = 0; k < S; ++k) { mbar_init(&full[k], 1); mbar_init(&empty[k], CW); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  for (int j = threadIdx.x; j < kp; j += blockDim.x) {
-    const int col = __ldg(P.pcols + j);
-    us[j] = col >= 0 ? v[col] : 0.0;
-  }
-  __syncthreads();
+  __syncthreads();                               // barriers initialised
   const int ra = (int)((long long)op.m * blockIdx.x / gridDim.x);
   const int rb = (int)((long long)op.m * (blockIdx.x + 1) / gridDim.x);
   const int nch = (rb - ra + L.rc - 1) / L.rc;
@@ -129,67 +132,83 @@ __global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engin
   double2 acc[Q];
 #pragma unroll
   for (int q = 0; q < Q; ++q) acc[q] = make_double2(0.0, 0.0);
-  if (warp == CW) {
-    // ------------------------------------------------------------ producer --
-    if (lane == 0) {
-      const bool ldx = fuse && c.xupd;
-      for (int it = 0; it < nch; ++it) {
-        const int s = it % S;
-        mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-        double* st = ring + (size_t)s * L.size;
-        const int r0 = ra + it * L.rc, r1 = min(rb, r0 + L.rc);
-        const uint32_t b_p = (uint32_t)(r1 - r0) * kp * 8u;
-        const int v0 = r0 & ~1, w0 = (n + r0) & ~1;
-        const uint32_t b_d = round_up16((uint32_t)(((r1 + 1) & ~1) - v0) * 8u);
-        const uint32_t b_w = round_up16((uint32_t)(((n + r1 + 1) & ~1) - w0) * 8u);
-        uint32_t b_e = 0, b_ec = 0;
-        long long e0 = 0, c0 = 0;
-        if (ew > 0) {
-          e0 = ((long long)r0 * ew) & ~1LL;
-          b_e = round_up16((uint32_t)((((long long)r1 * ew + 1) & ~1LL) - e0) * 8u);
-          if (!direct) {
-            c0 = ((long long)r0 * ew) & ~3LL;
-            b_ec = round_up16((uint32_t)((((long long)r1 * ew + 3) & ~3LL) - c0) * 4u);
-          }
-        }
-        mbar_expect_tx(&full[s], b_p + b_d + b_w + (fuse ? b_w : 0u) + (ldx ? b_w : 0u) + (direct ? 2u : 1u) * b_e + b_ec);
-        bulk_g2s(st, P.P + (size_t)r0 * kp, b_p, &full[s]);
-        bulk_g2s(st + L.o_d, op.d + v0, b_d, &full[s]);
-        bulk_g2s(st + L.o_w, v + w0, b_w, &full[s]);
-        if (fuse) bulk_g2s(st + L.o_r, E.r + w0, b_w, &full[s]);
-        if (ldx) bulk_g2s(st + L.o_x, xsrc + w0, b_w, &full[s]);
-        if (ew > 0) {
-          bulk_g2s(st + L.o_ev, P.ev + e0, b_e, &full[s]);
-          if (direct) bulk_g2s(st + L.o_ue, P.ue + e0, b_e, &full[s]);
-          else bulk_g2s(st + L.o_ec, P.eci + c0, b_ec, &full[s]);
-        }
+  // producer: lane 0 of warp 0 issues chunk `it` into stage it % S once the
+  // stage's previous chunk has been consumed by every warp
+  const bool ldx = fuse && c.xupd;
+  auto produce = [&](int it) {
+    if (it >= nch) return;
+    const int s = it % S;
+    mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+    double* st = ring + (size_t)s * L.size;
+    const int r0 = ra + it * L.rc, r1 = min(rb, r0 + L.rc);
+    const uint32_t b_p = (uint32_t)(r1 - r0) * kp * 8u;
+    const int v0 = r0 & ~1, w0 = (n + r0) & ~1;
+    const uint32_t b_d = round_up16((uint32_t)(((r1 + 1) & ~1) - v0) * 8u);
+    const uint32_t b_w = round_up16((uint32_t)(((n + r1 + 1) & ~1) - w0) * 8u);
+    uint32_t b_e = 0, b_ec = 0;
+    long long e0 = 0, c0 = 0;
+    if (ew > 0) {
+      e0 = ((long long)r0 * ew) & ~1LL;
+      b_e = round_up16((uint32_t)((((long long)r1 * ew + 1) & ~1LL) - e0) * 8u);
+      if (!direct) {
+        c0 = ((long long)r0 * ew) & ~3LL;
+        b_ec = round_up16((uint32_t)((((long long)r1 * ew + 3) & ~3LL) - c0) * 4u);
       }
     }
-  } else {
+    mbar_expect_tx(&full[s], b_p + b_d + b_w + (fuse ? b_w : 0u) + (ldx ? b_w : 0u) + (direct ? 2u : 1u) * b_e + b_ec);
+    bulk_g2s(st, P.P + (size_t)r0 * kp, b_p, &full[s]);
+    bulk_g2s(st + L.o_d, op.d + v0, b_d, &full[s]);
+    bulk_g2s(st + L.o_w, v + w0, b_w, &full[s]);
+    if (fuse) bulk_g2s(st + L.o_r, E.r + w0, b_w, &full[s]);
+    if (ldx) bulk_g2s(st + L.o_x, xsrc + w0, b_w, &full[s]);
+    if (ew > 0) {
+      bulk_g2s(st + L.o_ev, P.ev + e0, b_e, &full[s]);
+      if (direct) bulk_g2s(st + L.o_ue, P.ue + e0, b_e, &full[s]);
+      else bulk_g2s(st + L.o_ec, P.eci + c0, b_ec, &full[s]);
+    }
+  };
+  const bool producer = warp == 0 && lane == 0;
+  if (producer)
+    for (int k = 0; k < S - 1; ++k) produce(k);
+  {
     // ----------------------------------------------------------- consumers --
     double* xdst = E.x[c.xn];
     double* wv = v + n;
     const double* u = v;
+    // u_P in registers: lane holds elements 2 lane + 64 q (+1), as the rows
+    double2 ur[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = 64 * q + 2 * lane;
+      const int c0 = __ldg(P.pcols + j), c1 = __ldg(P.pcols + j + 1);
+      ur[q] = make_double2(c0 >= 0 ? u[c0] : 0.0, c1 >= 0 ? u[c1] : 0.0);
+    }
     for (int it = 0; it < nch; ++it) {
       const int s = it % S;
+      if (producer) produce(it + S - 1);
       mbar_wait(&full[s], (it / S) & 1);
       const double* st = ring + (size_t)s * L.size;
       const int r0 = ra + it * L.rc, r1 = min(rb, r0 + L.rc);
       const int v0 = r0 & ~1, w0 = (n + r0) & ~1;
       const long long e0 = ((long long)r0 * ew) & ~1LL, c0 = ((long long)r0 * ew) & ~3LL;
-      for (int g0 = warp * RPW; r0 + g0 < r1; g0 += CW * RPW) {
+      for (int g0 = warp * RPW; r0 + g0 < r1 && !P.probe; g0 += CW * RPW) {
         double sum[RPW], ea[RPW];
+        double2 av[RPW][Q];                        // the rows, read from shared memory once
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
           const bool ok = r0 + g0 + i < r1;
           const double* a = st + (size_t)(ok ? g0 + i : g0) * kp + 2 * lane;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) av[i][q] = *reinterpret_cast<const double2*>(a + 64 * q);
+        }
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+          const bool ok = r0 + g0 + i < r1;
           double s0 = 0.0, s1 = 0.0;
 #pragma unroll
           for (int q = 0; q < Q; ++q) {
-            const double2 av = *reinterpret_cast<const double2*>(a + 64 * q);
-            const double2 uu = *reinterpret_cast<const double2*>(us + 64 * q + 2 * lane);
-            s0 = fma(av.x, uu.x, s0);
-            s1 = fma(av.y, uu.y, s1);
+            s0 = fma(av[i][q].x, ur[q].x, s0);
+            s1 = fma(av[i][q].y, ur[q].y, s1);
           }
           sum[i] = s0 + s1;
           ea[i] = 0.0;
@@ -206,51 +225,66 @@ __global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engin
             sum[i] = fma(ea[i], ug, sum[i]);
           }
         }
+        // transposed reduction: with RPW = 2 the first butterfly level splits
+        // the warp into two half-warps, one per row, so both rows' scalar
+        // work (division included) runs side by side
+        double tr;
+        int mine;
+        if (RPW == 2) {
+          const bool hi = lane & 16;
+          tr = (hi ? sum[RPW - 1] : sum[0]) + __shfl_xor_sync(0xffffffffu, hi ? sum[0] : sum[RPW - 1], 16);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
+          for (int o = 8; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+          mine = hi ? 1 : 0;
+        } else {
+          tr = sum[0];
 #pragma unroll
-          for (int i = 0; i < RPW; ++i) sum[i] += __shfl_xor_sync(0xffffffffu, sum[i], o);
+          for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
+          mine = 0;
+        }
+        constexpr int GS = 32 / RPW;             // lanes per row group
+        const bool leader = (lane & (GS - 1)) == 0;
+        double zm = 0.0;
+        {
+          const int r = r0 + g0 + mine;
+          if (r < r1) {
+            const double t = tr;
+            const double dr = st[L.o_d + r - v0];
+            double wr = st[L.o_w + n + r - w0];
+            if (fuse) {
+              const double rres = st[L.o_r + n + r - w0];
+              const double zr = __dmul_rn(1.0 / dr, rres);
+              const double pn = (c.mode == MODE_RESTART) ? zr : __dadd_rn(zr, __dmul_rn(c.beta, wr));
+              if (leader) {
+                if (c.xupd) xdst[n + r] = __dadd_rn(st[L.o_x + n + r - w0], __dmul_rn(c.alpha_prev, wr));
+                wv[r] = pn;
+                rzb += rres * zr;
+              }
+              wr = pn;
+            }
+            zm = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
+            const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
+            if (leader) {
+              E.y[n + r] = yb;
+              pacc += t * zm + wr * yb;
+              if (!direct) E.zb[r] = zm;
+            }
+          }
+        }
         double z[RPW];
 #pragma unroll
-        for (int i = 0; i < RPW; ++i) {
-          const int r = r0 + g0 + i;
-          z[i] = 0.0;
-          if (r >= r1) continue;
-          const double t = sum[i];
-          const double dr = st[L.o_d + r - v0];
-          double wr = st[L.o_w + n + r - w0];
-          if (fuse) {
-            const double rres = st[L.o_r + n + r - w0];
-            const double zr = __dmul_rn(1.0 / dr, rres);
-            const double pn = (c.mode == MODE_RESTART) ? zr : __dadd_rn(zr, __dmul_rn(c.beta, wr));
-            if (lane == 0) {
-              if (c.xupd) xdst[n + r] = __dadd_rn(st[L.o_x + n + r - w0], __dmul_rn(c.alpha_prev, wr));
-              wv[r] = pn;
-              rzb += rres * zr;
-            }
-            wr = pn;
-          }
-          z[i] = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
-          const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
-          if (lane == 0) {
-            E.y[n + r] = yb;
-            pacc += t * z[i] + wr * yb;
-          }
-          if (direct) {
-            if (lane < ew) P.yrem[(long long)r * ew + lane] = z[i] * ea[i];
-          } else if (lane == 0) {
-            E.zb[r] = z[i];
-          }
+        for (int i = 0; i < RPW; ++i) z[i] = __shfl_sync(0xffffffffu, zm, i * GS);
+        if (direct && lane < ew) {
+#pragma unroll
+          for (int i = 0; i < RPW; ++i)
+            if (r0 + g0 + i < r1) P.yrem[(long long)(r0 + g0 + i) * ew + lane] = z[i] * ea[i];
         }
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-          const bool ok = r0 + g0 + i < r1;
-          const double* a = st + (size_t)(ok ? g0 + i : g0) * kp + 2 * lane;
 #pragma unroll
-          for (int q = 0; q < Q; ++q) {                // the row again from shared memory
-            const double2 av = *reinterpret_cast<const double2*>(a + 64 * q);
-            acc[q].x = fma(z[i], av.x, acc[q].x);
-            acc[q].y = fma(z[i], av.y, acc[q].y);
+          for (int q = 0; q < Q; ++q) {
+            acc[q].x = fma(z[i], av[i][q].x, acc[q].x);
+            acc[q].y = fma(z[i], av[i][q].y, acc[q].y);
           }
         }
       }
@@ -260,10 +294,8 @@ __global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engin
   }
   __syncwarp();
   __syncthreads();                               // every stage consumed: the ring is free
-  if (warp < CW) {
 #pragma unroll
-    for (int q = 0; q < Q; ++q) *reinterpret_cast<double2*>(ring + (size_t)warp * kp + 64 * q + 2 * lane) = acc[q];
-  }
+  for (int q = 0; q < Q; ++q) *reinterpret_cast<double2*>(ring + (size_t)warp * kp + 64 * q + 2 * lane) = acc[q];
   __syncthreads();
   for (int j = threadIdx.x; j < kp; j += blockDim.x) {
     double sum = 0.0;
@@ -280,9 +312,10 @@ __global__ void __launch_bounds__((QPK_PANEL_CW + 1) * 32, 1) k_slot_panel(Engin
 // out[pcols[j]] (+)= sum over CTAs of ppart[cta][j], in CTA order.  Block b
 // covers panel columns 32 b .. 32 b + 31; warp w sums CTAs w, w + 8, ...;
 // the 8 warp sums are then added in warp order.
-__global__ void __launch_bounds__(256) k_panel_comb(Engine E, double* out, int add, int par) {
-  __shared__ double ws[8][33];
+__global__ void __launch_bounds__(1024) k_panel_comb(Engine E, double* out, int add, int par) {
+  __shared__ double ws[32][33];
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
+  if (par >= 0 && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_mid = globaltimer_ns();
   const Panel& P = E.panel;
   const int nb = P.kp / 32;
   if ((int)blockIdx.x >= nb) {
@@ -295,25 +328,25 @@ __global__ void __launch_bounds__(256) k_panel_comb(Engine E, double* out, int a
     }
     return;
   }
+  // block b: panel columns 32 b .. 32 b + 31; warp w sums CTAs w, w + 32, ...
+  // (independent loads), then the 32 warp sums in warp order
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x * 32 + lane;
   double s0 = 0.0, s1 = 0.0;
-  if (j < P.kp) {
-    int g = warp;
-    for (; g + 8 < P.G; g += 16) {
-      s0 += P.ppart[(size_t)g * P.kp + j];
-      s1 += P.ppart[(size_t)(g + 8) * P.kp + j];
-    }
-    if (g < P.G) s0 += P.ppart[(size_t)g * P.kp + j];
+  int g = warp;
+  for (; g + 32 < P.G; g += 64) {
+    s0 += P.ppart[(size_t)g * P.kp + j];
+    s1 += P.ppart[(size_t)(g + 32) * P.kp + j];
   }
+  if (g < P.G) s0 += P.ppart[(size_t)g * P.kp + j];
   ws[warp][lane] = s0 + s1;
   __syncthreads();
-  if (warp == 0 && j < P.kp) {
-    double s = 0.0;
+  if (warp == 0) {
+    double sum = 0.0;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) s += ws[w][lane];
+    for (int w = 0; w < 32; ++w) sum += ws[w][lane];
     const int col = __ldg(P.pcols + j);
-    if (col >= 0) out[col] = add ? out[col] + s : s;
+    if (col >= 0) out[col] = add ? out[col] + sum : sum;
   }
 }
 

@@ -335,6 +335,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
 #define QPK_COMB_CHUNK 128
 __global__ void __launch_bounds__(QPK_BLOCK) k_comb_seg(Engine E, int par) {
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
+  if (par >= 0 && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_mid = globaltimer_ns();
   const int LC = E.dict.comb_lanes, lc = threadIdx.x & (LC - 1);
   const int per = 32 / LC, sw = (threadIdx.x & 31) / LC;
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;

@@ -7,10 +7,10 @@ set -u
 mkdir -p gpurun_out
 NCU=${NCU:-ncu}
 for w in $1; do
-  iters=20
+  iters=200
   [ "$w" = cfg5 ] && iters=20
   $NCU --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
-       -s 300 -c 80 --csv --log-file gpurun_out/t_$w.csv \
+       -s 100 -c 60 --csv --log-file gpurun_out/t_$w.csv \
        python bench.py --workload $w --steps 1 --warmup 3 --iters $iters --no-cpu-baseline \
        > gpurun_out/t_$w.log 2>&1
   echo "$w metrics rc=$?"
