@@ -350,6 +350,8 @@ def run_ours(args):
                        "working set fits L2 (each step re-reads it every PCG iteration; no flush)",
                        "n": op.n, "m_B": op.m, "nnz_B": gk.ctx.query("nnz"),
                        "grid": gk.ctx.query("grid"), "lanes_per_row": gk.ctx.query("lanes"),
+                       "hess_tiled": gk.ctx.query("hess_tiled"), "tile_cta_acc": gk.ctx.query("tile_cta_acc"),
+                       "panel_cols": gk.ctx.query("panel_cols"),
                        "engine": "slot engine (per-phase kernels, CUDA graph)" if engine_used else
                                  "persistent cooperative kernel",
                        "seed": meta["seed"]},

@@ -498,6 +498,13 @@ struct qpk_ctx {
   DBuf<double> comb_sum;
   int comb_lanes = 8, comb_nseg = 0;
   DBuf<TileDescD> tiles;
+  DBuf<int> hperm;                // Hessian tile row q -> H row hperm[q] (RCM order)
+  // CTA-level accumulation of the tile partials (Dict::cacc)
+  bool cacc = false;
+  int tile_grid = 0;
+  DBuf<int> tile_beg, cta_off, tslot, col_ptr2, col_pos2, comb_beg2, comb_col2;
+  DBuf<double> cpart;
+  int comb_lanes2 = 8, comb_nseg2 = 0;
   DBuf<double> tval;
   DBuf<int4> rtile_desc;
   int n_rtiles = 0;
@@ -575,6 +582,7 @@ static cudaError_t upload(DBuf<T>& dst, const std::vector<T>& src, cudaStream_t 
 
 static int engine_setup(qpk_ctx* c);
 static Engine make_engine(qpk_ctx* c);
+static size_t tile_smem() { return sizeof(DTileSmem) + (size_t)QPK_TILE_GROUPS * QPK_TILE_UMAX * sizeof(double); }
 
 // ---------------------------------------------------------- dispatchers ---
 template <int L, bool CSC>
@@ -877,6 +885,53 @@ static int build_csc(qpk_ctx* c, const std::vector<int>& h_rp, const std::vector
   return QPK_OK;
 }
 
+// Reverse Cuthill-McKee order of a symmetric sparsity pattern (rows of H):
+// BFS from a pseudo-peripheral vertex of each component, neighbours by
+// increasing degree, reversed.  Returns perm[new position] = old row.
+static std::vector<int> rcm_order(long long n, const std::vector<int>& rp, const std::vector<int>& ci) {
+  std::vector<int> order, deg(n), level(n, -1), nb;
+  order.reserve(n);
+  for (long long i = 0; i < n; ++i) deg[i] = rp[i + 1] - rp[i];
+  std::vector<char> done(n, 0);
+  auto bfs_last = [&](int s) {                       // farthest vertex from s (level structure)
+    std::vector<int> q{s};
+    level[s] = 0;
+    int last = s;
+    for (size_t h = 0; h < q.size(); ++h) {
+      const int x = q[h];
+      last = x;
+      for (int k = rp[x]; k < rp[x + 1]; ++k) {
+        const int y = ci[k];
+        if (y >= 0 && y < n && level[y] < 0) { level[y] = level[x] + 1; q.push_back(y); }
+      }
+    }
+    for (int x : q) level[x] = -1;
+    return last;
+  };
+  std::vector<int> idx(n);
+  for (long long i = 0; i < n; ++i) idx[i] = (int)i;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+  for (int s0 : idx) {
+    if (done[s0]) continue;
+    const int s = bfs_last(bfs_last(s0));
+    const size_t head0 = order.size();
+    order.push_back(s);
+    done[s] = 1;
+    for (size_t h = head0; h < order.size(); ++h) {
+      const int x = order[h];
+      nb.clear();
+      for (int k = rp[x]; k < rp[x + 1]; ++k) {
+        const int y = ci[k];
+        if (y >= 0 && y < n && !done[y]) { done[y] = 1; nb.push_back(y); }
+      }
+      std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+      for (int y : nb) order.push_back(y);
+    }
+  }
+  std::reverse(order.begin(), order.end());
+  return order;
+}
+
 // Dense row tiles: consecutive rows grouped while (rows x padded distinct
 // columns) fits QPK_TILE_DOUBLES, each tile stored as a dense block over its
 // sorted column list.  have_dict = false when a single row is too wide.
@@ -893,21 +948,23 @@ static int build_dict(qpk_ctx* c) {
   auto r4 = [](long long x) { return (x + 3) & ~3LL; };
   // tile the rows [0, nrows) of a CSR matrix; returns dense slots, or -1 if a
   // row is wider than a tile
-  auto tile_rows = [&](const int* rp, const int* ci, const double* v, long long nrows, int kind) -> long long {
+  auto tile_rows = [&](const int* rp, const int* ci, const double* v, long long nrows, int kind,
+                       const int* perm) -> long long {
     long long slots = 0, r = 0;
+    auto R = [&](long long q) -> long long { return perm ? perm[q] : q; };
     while (r < nrows) {
       const long long ra = r;
       cur.clear();
       while (r < nrows) {
         long long fresh = 0;
-        for (int k = rp[r]; k < rp[r + 1]; ++k)
+        for (int k = rp[R(r)]; k < rp[R(r) + 1]; ++k)
           if (ci[k] >= 0 && mark[ci[k]] != tid) ++fresh;
         const long long nd = (long long)cur.size() + fresh, rows = r - ra + 1;
         if (r4(nd) > QPK_TILE_DMAX || rows * (r4(nd) | 1) > QPK_TILE_DOUBLES || rows > QPK_TILE_ROWS) {
           if (r == ra) return -1;
           break;
         }
-        for (int k = rp[r]; k < rp[r + 1]; ++k)
+        for (int k = rp[R(r)]; k < rp[R(r) + 1]; ++k)
           if (ci[k] >= 0 && mark[ci[k]] != tid) { mark[ci[k]] = tid; cur.push_back(ci[k]); }
         ++r;
       }
@@ -924,7 +981,7 @@ static int build_dict(qpk_ctx* c) {
       const size_t base = td.v0;
       tval.resize(base + (size_t)(r - ra) * pitch, 0.0);
       for (long long rr = ra; rr < r; ++rr)
-        for (int k = rp[rr]; k < rp[rr + 1]; ++k) {
+        for (int k = rp[R(rr)]; k < rp[R(rr) + 1]; ++k) {
           if (ci[k] < 0) continue;
           const int pos = (int)(std::lower_bound(cur.begin(), cur.end(), ci[k]) - cur.begin());
           tval[base + (size_t)(rr - ra) * pitch + pos] = v[k];
@@ -935,7 +992,7 @@ static int build_dict(qpk_ctx* c) {
     }
     return slots;
   };
-  const long long slots = tile_rows(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), m, 0);
+  const long long slots = tile_rows(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), m, 0, nullptr);
   if (slots < 0) return QPK_OK;
   const size_t n_bcols = cols.size();
   const int n_btiles = tid;
@@ -943,9 +1000,18 @@ static int build_dict(qpk_ctx* c) {
   // when they are dense enough -- the owner rank only
   if (c->hkind == QPK_HESS_CSR && c->rank == 0 && !c->h_hci.empty()) {
     const size_t t0 = tiles.size(), c0 = cols.size(), v0 = tval.size();
-    const long long hs = tile_rows(c->h_hrp.data(), c->h_hci.data(), c->h_hv.data(), n, 1);
+    // rows in reverse Cuthill-McKee order: a Hessian like D_t'D_t of randomly
+    // numbered band columns is banded in that order, so consecutive rows share
+    // their columns and the tiles come out dense (tile row q is H row hperm[q])
+    std::vector<int> hperm = rcm_order(n, c->h_hrp, c->h_hci);
+    // empty rows (columns that never meet the objective block) need no tile
+    hperm.erase(std::remove_if(hperm.begin(), hperm.end(),
+                               [&](int j) { return c->h_hrp[j + 1] == c->h_hrp[j]; }), hperm.end());
+    const long long hs = tile_rows(c->h_hrp.data(), c->h_hci.data(), c->h_hv.data(), (long long)hperm.size(), 1,
+                                   hperm.data());
     if (hs > 0 && (double)c->h_hci.size() / (double)hs >= 0.5) {
       c->h_tiled = true;
+      CUDA_TRY(upload(c->hperm, hperm, c->stream));
     } else {
       tiles.resize(t0); cols.resize(c0); tval.resize(v0); tid = n_btiles;
     }
@@ -975,6 +1041,68 @@ static int build_dict(qpk_ctx* c) {
     CUDA_TRY(upload(c->comb_beg, cbeg, c->stream));
     CUDA_TRY(c->comb_sum.alloc(std::max(c->comb_nseg, 1)));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
+  // CTA-level accumulation: CTA b runs a consecutive, slot-balanced range of
+  // tiles and sums their partials per column of the range's union in shared
+  // memory; the combine then reads ~one partial per (CTA, column)
+  c->cacc = false;
+  if (!getenv("QPK_NO_CACC")) {
+    const int G = std::max(1, std::min(c->sms, tid));
+    std::vector<long long> pre(tid + 1, 0);
+    // weight = dense slots + a fixed per-tile cost (barriers, copies) of ~2k slots
+    for (int t = 0; t < tid; ++t) pre[t + 1] = pre[t] + (long long)(tiles[t].rb - tiles[t].ra) * tiles[t].pad0 + 2048;
+    std::vector<int> tbeg(G + 1, 0);
+    for (int b = 1; b < G; ++b)
+      tbeg[b] = (int)(std::lower_bound(pre.begin(), pre.end(), pre[tid] * b / G) - pre.begin());
+    tbeg[G] = tid;
+    for (int b = 1; b <= G; ++b) tbeg[b] = std::max(tbeg[b], tbeg[b - 1]);
+    std::vector<int> seen(n, -1), slot_of(n, 0), off(G + 1, 0), ucols, tsl(cols.size(), -1);
+    bool ok = true;
+    for (int b = 0; b < G && ok; ++b) {
+      int cnt = 0;
+      for (int t = tbeg[b]; t < tbeg[b + 1]; ++t) {
+        if (tiles[t].pad1) continue;                      // Hessian tiles write y directly
+        for (int cc = 0; cc < tiles[t].ndp; ++cc) {
+          const int col = cols[tiles[t].d0 + cc];
+          if (col < 0) continue;
+          if (seen[col] != b) { seen[col] = b; slot_of[col] = cnt++; ucols.push_back(col); }
+          tsl[tiles[t].d0 + cc] = slot_of[col];
+        }
+      }
+      if (cnt > QPK_TILE_UMAX) ok = false;
+      off[b + 1] = off[b] + cnt;
+    }
+    if (ok) {
+      // column j -> its CTA partial positions, in CTA order
+      std::vector<int> cp2(n + 1, 0), cpos2((size_t)off[G]);
+      for (int col : ucols) cp2[col + 1]++;
+      for (long long j = 0; j < n; ++j) cp2[j + 1] += cp2[j];
+      std::vector<int> at(cp2.begin(), cp2.end() - 1);
+      for (int q = 0; q < off[G]; ++q) cpos2[at[ucols[q]]++] = q;
+      std::vector<int> cseg(n + 1, 0), cbeg;
+      for (long long j = 0; j < n; ++j) {
+        cseg[j] = (int)cbeg.size();
+        for (int b = cp2[j]; b < cp2[j + 1]; b += QPK_COMB_CHUNK) cbeg.push_back(b);
+      }
+      cseg[n] = (int)cbeg.size();
+      cbeg.push_back(cp2[n]);
+      c->comb_nseg2 = cseg[n];
+      const long long avg = (long long)cpos2.size() / std::max<long long>(c->comb_nseg2, 1);
+      c->comb_lanes2 = pow2_clamp((avg + 3) / 4, 1, 32);
+      tsl.resize(tsl.size() + 16, -1);
+      CUDA_TRY(upload(c->tile_beg, tbeg, c->stream));
+      CUDA_TRY(upload(c->cta_off, off, c->stream));
+      CUDA_TRY(upload(c->tslot, tsl, c->stream));
+      CUDA_TRY(upload(c->col_ptr2, cp2, c->stream));
+      CUDA_TRY(upload(c->col_pos2, cpos2, c->stream));
+      CUDA_TRY(upload(c->comb_col2, cseg, c->stream));
+      CUDA_TRY(upload(c->comb_beg2, cbeg, c->stream));
+      CUDA_TRY(c->cpart.alloc(std::max(off[G], 1)));
+      CUDA_TRY(c->comb_sum.alloc(std::max(std::max(c->comb_nseg, c->comb_nseg2), 1)));
+      CUDA_TRY(cudaStreamSynchronize(c->stream));
+      c->cacc = true;
+      c->tile_grid = G;
+    }
   }
   cols.resize(cols.size() + 16, -1);                  // bulk copies read 16-byte windows
   tval.resize(tval.size() + 16, 0.0);
@@ -1196,6 +1324,8 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     if (c->scatter == QPK_SCATTER_PANEL) ework = std::max<long long>(2 * c->sms, N / 1024);
     if (const char* ev = getenv("QPK_ENGINE_GRID")) ework = atoi(ev);
     c->grid_eng = (int)std::max<long long>(1, std::min<long long>((long long)eng_per_sm * c->sms, ework));
+    // the partial-sum stride E.G must cover every kernel's blocks (tile CTAs included)
+    if (c->scatter == QPK_SCATTER_DICT && c->cacc) c->grid_eng = std::max(c->grid_eng, c->tile_grid);
   }
   if (c->scatter == QPK_SCATTER_PANEL) {
     c->panel_grid = std::max(1, std::min(c->sms, c->grid_eng));      // one CTA per SM
@@ -1273,6 +1403,11 @@ static int build_jacobi(qpk_ctx* c) {
     int rc = engine_setup(c);
     if (rc) return rc;
     Engine E = make_engine(c);
+    // per-tile partials (strided tiles) and their combine structures
+    E.dict.cacc = 0;
+    E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
+    E.dict.comb_lanes = c->comb_lanes; E.dict.nseg = c->comb_nseg;
+    E.dict.seg_beg = c->comb_beg.p; E.dict.col_seg = c->comb_col.p;
     k_jac_tile<<<c->grid_eng, QPK_BLOCK, 0, s>>>(E);
     // column sums of the tile partials (sharded: summed over ranks), then the common finish
     k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, -1);
@@ -1407,7 +1542,7 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   } else if (c->scatter == QPK_SCATTER_DICT) {
     k_slot_rows_tile<<<E.G_rows, (QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32,
-                       sizeof(DTileSmem), s>>>(E, par);
+                       tile_smem(), s>>>(E, par);
     k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, par);               // y_top += B'z (tile partials)
     k_comb_col<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);
     if (c->hkind != QPK_HESS_DIAG && !c->h_tiled) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
@@ -1501,13 +1636,23 @@ static Engine make_engine(qpk_ctx* c) {
   E.dict.comb_lanes = c->comb_lanes;
   E.dict.nseg = c->comb_nseg; E.dict.seg_beg = c->comb_beg.p; E.dict.col_seg = c->comb_col.p;
   E.dict.seg_sum = c->comb_sum.p;
+  E.dict.hperm = c->h_tiled ? c->hperm.p : nullptr;
+  E.dict.cacc = 0;
+  if (c->scatter == QPK_SCATTER_DICT && c->cacc) {
+    E.dict.cacc = 1;
+    E.dict.tile_beg = c->tile_beg.p; E.dict.cta_off = c->cta_off.p; E.dict.tslot = c->tslot.p;
+    E.dict.cpart = c->cpart.p;
+    E.dict.col_ptr = c->col_ptr2.p; E.dict.col_pos = c->col_pos2.p;
+    E.dict.comb_lanes = c->comb_lanes2; E.dict.nseg = c->comb_nseg2;
+    E.dict.seg_beg = c->comb_beg2.p; E.dict.col_seg = c->comb_col2.p;
+    E.G_rows = c->tile_grid;
+  }
   return E;
 }
 
 static int engine_setup(qpk_ctx* c) {
   if (c->ctrl.p) return QPK_OK;
-  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sizeof(DTileSmem)));
+  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem()));
   if (c->scatter == QPK_SCATTER_PANEL) CUDA_TRY(panel_attr(c));
   CUDA_TRY(c->ctrl.alloc(2));
   CUDA_TRY(c->gscal.alloc(4));
@@ -1942,6 +2087,7 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "dict_blocks") return c->nblk;
   if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "hess_tiled") return c->h_tiled ? 1 : 0;
+  if (k == "tile_cta_acc") return c->cacc ? 1 : 0;
   if (k == "panel_kp") return c->panel_kp;
   if (k == "panel_cols") return c->panel_kd;
   if (k == "panel_ew") return c->panel_ew;

@@ -68,6 +68,18 @@ struct Dict {
   const int* seg_beg;        // segment q: col_pos[seg_beg[q] .. seg_beg[q+1])
   const int* col_seg;        // column j: segments [col_seg[j], col_seg[j+1])
   double* seg_sum;
+  // CTA-level accumulation (cacc = 1): CTA b runs the consecutive tiles
+  // [tile_beg[b], tile_beg[b+1]) and sums their B'z partials in shared memory
+  // per column of its union cta_cols (tile column c -> slot tslot[d0 + c]),
+  // written once to cpart[cta_off[b] ..]; the combine then reads these few
+  // CTA partials (through the same segment structures) instead of one
+  // partial per tile and column.
+  const int* hperm;          // Hessian tiles: tile row q is H row hperm[q] (null: identity)
+  int cacc;
+  const int* tile_beg;
+  const int* cta_off;
+  const int* tslot;
+  double* cpart;
 };
 
 // Dense column panel (the "panel" mode, for B with a block of dense columns --
@@ -317,7 +329,8 @@ __device__ __forceinline__ double top_value(const Engine& E, int j) {
     for (int q = qb; q < qe; ++q) s += E.seg_sum[q];
   } else if (SC == 3) {
     const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
-    for (int q = qb; q < qe; ++q) s += E.dict.bpart[__ldg(E.dict.col_pos + q)];
+    const double* src = E.dict.cacc ? E.dict.cpart : E.dict.bpart;
+    for (int q = qb; q < qe; ++q) s += src[__ldg(E.dict.col_pos + q)];
   }
   return E.y[j] + s;
 }

@@ -85,6 +85,7 @@ struct alignas(16) DTileStage {
 #endif
 #define QPK_TILE_GWARPS 4        // warps per consumer group
 #define QPK_TILE_GATHER_WARPS 2  // warps gathering u[cols] for landed tiles
+#define QPK_TILE_UMAX 1536       // CTA-accumulator capacity (distinct columns of a CTA's tiles)
 
 struct DTileSmem {
   DTileStage st[QPK_TILE_STAGES];
@@ -110,6 +111,7 @@ __global__ void __launch_bounds__((QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_T
 k_slot_rows_tile(Engine E, int par) {
   extern __shared__ __align__(128) unsigned char smraw[];
   DTileSmem& S = *reinterpret_cast<DTileSmem*>(smraw);
+  double* cacc = reinterpret_cast<double*>(smraw + sizeof(DTileSmem));   // [GROUPS][UMAX] (cacc mode)
   constexpr int CW = QPK_TILE_GROUPS * QPK_TILE_GWARPS;   // consumer warps
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
@@ -127,8 +129,15 @@ k_slot_rows_tile(Engine E, int par) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // tiles of this CTA: consecutive (cacc) or strided
+  const int tb = D.cacc ? __ldg(D.tile_beg + blockIdx.x) : (int)blockIdx.x;
+  const int tstep = D.cacc ? 1 : (int)gridDim.x;
+  const int my = D.cacc ? __ldg(D.tile_beg + blockIdx.x + 1) - tb
+                        : ((D.nblk > (int)blockIdx.x) ? (D.nblk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0);
+  const int nu = D.cacc ? __ldg(D.cta_off + blockIdx.x + 1) - __ldg(D.cta_off + blockIdx.x) : 0;
+  for (int i = threadIdx.x; i < QPK_TILE_GROUPS * nu; i += blockDim.x)
+    cacc[(i / nu) * QPK_TILE_UMAX + (i % nu)] = 0.0;
   __syncthreads();
-  const int my = (D.nblk > (int)blockIdx.x) ? (D.nblk - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   double pacc = 0.0, rzb = 0.0;
   if (warp == CW) {
     // ---------------------------------------------------------- producer ----
@@ -136,7 +145,7 @@ k_slot_rows_tile(Engine E, int par) {
       const double* wsrc = v;
       const double* xsrc = E.x[c.cur];
       for (int it = 0; it < my; ++it) {
-        const int t = blockIdx.x + it * gridDim.x;
+        const int t = tb + it * tstep;
         const int s = it % QPK_TILE_STAGES;
         mbar_wait(&S.empty[s], ((it / QPK_TILE_STAGES) & 1) ^ 1);
         DTileStage& st = S.st[s];
@@ -177,20 +186,31 @@ k_slot_rows_tile(Engine E, int par) {
       mbar_wait(&S.full[s], (it / QPK_TILE_STAGES) & 1);
       DTileStage& st = S.st[s];
       const int nd = st.t.ndp;
+      // (CTA accumulation: the tile's column list is no longer needed once
+      // gathered, so its slots in the CTA accumulator replace it in place)
+      const bool slots = D.cacc && !st.t.pad1;
+      const int d0 = st.t.d0;
       for (int cb = lane; cb < nd; cb += 32 * 8) {
         double g8[8];
+        int s8[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int cc = cb + 32 * q;
           const int col = cc < nd ? st.cols[cc] : -1;
           g8[q] = col >= 0 ? u[col] : 0.0;
+          s8[q] = (slots && cc < nd) ? __ldg(D.tslot + d0 + cc) : -1;
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int cc = cb + 32 * q;
-          if (cc < nd) st.ud[cc] = g8[q];
+          if (cc < nd) {
+            st.ud[cc] = g8[q];
+            if (slots) st.cols[cc] = s8[q];
+          }
         }
       }
+      // generic-proxy writes into a stage the TMA (async proxy) refills later
+      if (slots) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.uready[s]);
     }
@@ -229,7 +249,7 @@ k_slot_rows_tile(Engine E, int par) {
           double tt = 0.0;
 #pragma unroll
           for (int ww = 0; ww < QPK_TILE_GWARPS; ++ww) tt += S.rpart[g][ww][rr];
-          const int j = td.ra + rr;
+          const int j = D.hperm ? __ldg(D.hperm + td.ra + rr) : td.ra + rr;
           E.y[j] += tt;
           pacc += v[j] * tt;
         }
@@ -269,13 +289,27 @@ k_slot_rows_tile(Engine E, int par) {
           s1 = fma(st.a[(rr + 1) * pitch + cc], S.zs[g][rr + 1], s1);
         }
         if (rr < R) s0 = fma(st.a[rr * pitch + cc], S.zs[g][rr], s0);
-        D.bpart[td.d0 + cc] = s0 + s1;
+        if (D.cacc) {
+          const int sl = st.cols[cc];                     // slot (gather warps), distinct per tile column
+          if (sl >= 0) cacc[g * QPK_TILE_UMAX + sl] += s0 + s1;
+        } else {
+          D.bpart[td.d0 + cc] = s0 + s1;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.empty[s]);
     }
   }
   __syncthreads();
+  if (D.cacc) {                                       // CTA partials, groups added in order
+    const int off = __ldg(D.cta_off + blockIdx.x);
+    for (int u = threadIdx.x; u < nu; u += blockDim.x) {
+      double sum = 0.0;
+#pragma unroll
+      for (int g = 0; g < QPK_TILE_GROUPS; ++g) sum += cacc[g * QPK_TILE_UMAX + u];
+      D.cpart[off + u] = sum;
+    }
+  }
   // (the non-diagonal Hessian part runs in k_slot_hess: more blocks than this grid)
   double t = block_sum(pacc, S.red);
   if (threadIdx.x == 0) E.part[SLOT_ROWS * E.G + blockIdx.x] = t;
@@ -345,11 +379,12 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_comb_seg(Engine E, int par) {
     if (q < E.dict.nseg) {
       const int b = __ldg(E.dict.seg_beg + q), e = __ldg(E.dict.seg_beg + q + 1);
       int k = b + lc;
+      const double* src = E.dict.cacc ? E.dict.cpart : E.dict.bpart;
       for (; k + LC < e; k += 2 * LC) {
-        s0 += E.dict.bpart[__ldg(E.dict.col_pos + k)];
-        s1 += E.dict.bpart[__ldg(E.dict.col_pos + k + LC)];
+        s0 += src[__ldg(E.dict.col_pos + k)];
+        s1 += src[__ldg(E.dict.col_pos + k + LC)];
       }
-      if (k < e) s0 += E.dict.bpart[__ldg(E.dict.col_pos + k)];
+      if (k < e) s0 += src[__ldg(E.dict.col_pos + k)];
     }
     double sum = s0 + s1;
     for (int o = LC / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
