@@ -28,6 +28,7 @@
 #include "qpk_engine.cuh"
 #include "qpk_tma.cuh"
 #include "qpk_panel.cuh"
+#include "qpk_cluster.cuh"
 #include "qpk_ipm.cuh"
 #include <chrono>
 
@@ -529,6 +530,12 @@ struct qpk_ctx {
   DBuf<double> x[3], r, p, y, zb, rhs, part, hist, vin;
   DBuf<PcgOut> out;
   int grid_pcg = 0, grid_std = 0;
+  // small systems: the whole solve in one thread-block cluster (qpk_cluster.cuh)
+  int cl_C = 0;                    // 0: not used
+  size_t cl_smem = 0;
+  DBuf<ClCta> cl_ctas;
+  DBuf<unsigned char> cl_blob;
+  DBuf<long long> cl_off;
 
   // device-resident IPM (qpk_ipm_*)
   bool ipm_ready = false;
@@ -1211,6 +1218,118 @@ static int build_panel(qpk_ctx* c, bool force) {
   return QPK_OK;
 }
 
+// Small systems: split B's rows and H's rows over C CTAs of one cluster and
+// pack each CTA's slice (CSR + CSC of its B rows, CSR of its H rows) into a
+// blob the kernel copies to shared memory.  Eligible when every slice fits
+// (QPK_CL_SMEM) and H is diagonal, sparse or dense.
+static int build_cluster(qpk_ctx* c) {
+  c->cl_C = 0;
+  if (getenv("QPK_NO_CLUSTER") || c->sharded || c->hkind == QPK_HESS_LOWRANK) return QPK_OK;
+  const long long n = c->n, m = c->m;
+  if (n > 16384 || (long long)c->h_ci.size() > 4000000) return QPK_OK;
+  // H as full CSR rows
+  std::vector<int> hrp(n + 1, 0), hci;
+  std::vector<double> hv;
+  if (c->hkind == QPK_HESS_DIAG) {
+    for (long long j = 0; j < n; ++j) { hci.push_back((int)j); hv.push_back(c->h_h[j]); hrp[j + 1] = (int)hci.size(); }
+  } else if (c->hkind == QPK_HESS_DENSE) {
+    for (long long j = 0; j < n; ++j) {
+      for (long long k = 0; k < n; ++k) { hci.push_back((int)k); hv.push_back(c->h_dense[j * n + k]); }
+      hrp[j + 1] = (int)hci.size();
+    }
+  } else {
+    hrp = c->h_hrp; hci = c->h_hci; hv = c->h_hv;
+  }
+  auto align16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
+  int C = m >= 128 ? 16 : std::max(2, pow2_clamp((m + 7) / 8, 2, 16));
+  for (; C <= QPK_CL_MAXC; C *= 2) {
+    // contiguous splits balanced by nonzeros (B rows) and by nonzeros (H rows)
+    std::vector<int> rsp(C + 1, 0), hsp(C + 1, 0);
+    const long long nzb = c->h_rp[m];
+    for (int k = 1; k < C; ++k) {
+      long long target = nzb * k / C;
+      rsp[k] = (int)(std::lower_bound(c->h_rp.begin(), c->h_rp.begin() + m + 1, (int)target) - c->h_rp.begin());
+      rsp[k] = std::max(rsp[k], rsp[k - 1]);
+      const long long nzh = hrp[n];
+      target = nzh * k / C;
+      hsp[k] = (int)(std::lower_bound(hrp.begin(), hrp.end(), (int)target) - hrp.begin());
+      hsp[k] = std::max(hsp[k], hsp[k - 1]);
+    }
+    rsp[C] = (int)m; hsp[C] = (int)n;
+    std::vector<ClCta> ctas(C);
+    std::vector<unsigned char> blob;
+    std::vector<long long> off(C);
+    size_t worst = 0;
+    for (int k = 0; k < C; ++k) {
+      ClCta& t = ctas[k];
+      t.r0 = rsp[k]; t.r1 = rsp[k + 1]; t.h0 = hsp[k]; t.h1 = hsp[k + 1];
+      const int mr = t.r1 - t.r0, nh = t.h1 - t.h0;
+      // B slice CSR (skip the padding entries of the padded CSR)
+      std::vector<int> brp(mr + 1, 0), bci, ccp(n + 1, 0), cri;
+      std::vector<double> bv, cv;
+      for (int r = t.r0; r < t.r1; ++r) {
+        for (int q = c->h_rp[r]; q < c->h_rp[r + 1]; ++q)
+          if (c->h_ci[q] >= 0) { bci.push_back(c->h_ci[q]); bv.push_back(c->h_v[q]); }
+        brp[r - t.r0 + 1] = (int)bci.size();
+      }
+      for (int col : bci) ccp[col + 1]++;
+      for (long long j = 0; j < n; ++j) ccp[j + 1] += ccp[j];
+      cri.resize(bci.size()); cv.resize(bci.size());
+      {
+        std::vector<int> at(ccp.begin(), ccp.end() - 1);
+        for (int rr = 0; rr < mr; ++rr)
+          for (int q = brp[rr]; q < brp[rr + 1]; ++q) { const int a = at[bci[q]]++; cri[a] = rr; cv[a] = bv[q]; }
+      }
+      const int nnzh = hrp[t.h1] - hrp[t.h0];
+      std::vector<int> lhrp(nh + 1);
+      for (int j = 0; j <= nh; ++j) lhrp[j] = hrp[t.h0 + j] - hrp[t.h0];
+      t.nnzb = (int)bci.size(); t.nnzh = nnzh;
+      size_t o = 0;
+      auto place = [&](size_t bytes) { const size_t at = o; o = align16(o + bytes); return (int)at; };
+      t.o_brp = place((mr + 1) * 4); t.o_bci = place(bci.size() * 4); t.o_bv = place(bv.size() * 8);
+      t.o_ccp = place((n + 1) * 4); t.o_cri = place(cri.size() * 4); t.o_cv = place(cv.size() * 8);
+      t.o_hrp = place((nh + 1) * 4); t.o_hci = place((size_t)nnzh * 4); t.o_hv = place((size_t)nnzh * 8);
+      t.bytes = (int)align16(o); t.pad = 0;
+      const size_t need = cl_layout((int)n, mr, nh, t.bytes).bytes;
+      worst = std::max(worst, need);
+      if (need > QPK_CL_SMEM) break;
+      off[k] = (long long)blob.size();
+      blob.resize(blob.size() + t.bytes, 0);
+      unsigned char* b = blob.data() + off[k];
+      auto put = [&](int at, const void* src, size_t bytes) { if (bytes) memcpy(b + at, src, bytes); };
+      put(t.o_brp, brp.data(), brp.size() * 4); put(t.o_bci, bci.data(), bci.size() * 4);
+      put(t.o_bv, bv.data(), bv.size() * 8); put(t.o_ccp, ccp.data(), ccp.size() * 4);
+      put(t.o_cri, cri.data(), cri.size() * 4); put(t.o_cv, cv.data(), cv.size() * 8);
+      put(t.o_hrp, lhrp.data(), lhrp.size() * 4); put(t.o_hci, hci.data() + hrp[t.h0], (size_t)nnzh * 4);
+      put(t.o_hv, hv.data() + hrp[t.h0], (size_t)nnzh * 8);
+    }
+    if (worst > QPK_CL_SMEM) continue;
+    // can the device co-schedule a cluster of C CTAs with this much shared memory?
+    if (C > 8) cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_pcg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, QPK_CL_SMEM);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(C); lc.blockDim = dim3(QPK_CL_THREADS); lc.dynamicSmemBytes = worst;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    lc.attrs = at; lc.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, (void*)k_pcg_cluster, &lc) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      return QPK_OK;                                   // larger clusters will not fit either
+    }
+    blob.resize(blob.size() + 16, 0);
+    CUDA_TRY(upload(c->cl_ctas, ctas, c->stream));
+    CUDA_TRY(upload(c->cl_blob, blob, c->stream));
+    CUDA_TRY(upload(c->cl_off, off, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->cl_C = C;
+    c->cl_smem = worst;
+    return QPK_OK;
+  }
+  return QPK_OK;
+}
+
 int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_finalize: no problem being built");
   const long long mB = c->m_e + c->m_l + c->m_u;
@@ -1334,6 +1453,10 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   CUDA_TRY(c->part.alloc((size_t)NSLOTS * std::max(c->grid_pcg, c->grid_eng)));
   if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
 
+  {
+    int rc = build_cluster(c);
+    if (rc) return rc;
+  }
   Op o = c->op();
   k_hdiag<<<std::max(1, std::min(c->sms * 4, (int)((c->n + 255) / 256))), 256, 0, s>>>(o.H, (int)c->n, c->hdiag.p);
   c->launches++;
@@ -1769,6 +1892,25 @@ static int pcg_impl(qpk_ctx* c, const double* rhs_dev, double tol, int rel, int6
     int rc = pcg_engine(c, tol, rel, max_iters, hist_dev, &o);
     if (rc) return rc;
     CUDA_TRY(cudaEventRecord(e1, c->stream));
+  } else if (c->cl_C > 0) {
+    ClParams P;
+    P.n = (int)c->n; P.m = (int)c->m; P.C = c->cl_C;
+    P.ctas = c->cl_ctas.p; P.blob = c->cl_blob.p; P.blob_off = c->cl_off.p;
+    P.q = c->q.p; P.d = c->d.p; P.minv = c->minv.p; P.rhs = c->rhs.p;
+    P.x_out = c->x[0].p; P.hist = hist_dev;
+    P.tol = tol; P.rel = rel ? 1 : 0; P.max_iters = max_iters;
+    P.out = c->out.p;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(c->cl_C); lc.blockDim = dim3(QPK_CL_THREADS); lc.dynamicSmemBytes = c->cl_smem;
+    lc.stream = c->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->cl_C; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    lc.attrs = at; lc.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&lc, k_pcg_cluster, P));
+    c->launches++;
+    CUDA_TRY(cudaEventRecord(e1, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(&o, c->out.p, sizeof o, cudaMemcpyDeviceToHost, c->stream));
   } else {
     PcgParams P;
     P.op = c->op();
@@ -2087,6 +2229,7 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "dict_blocks") return c->nblk;
   if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "hess_tiled") return c->h_tiled ? 1 : 0;
+  if (k == "cluster") return c->cl_C;
   if (k == "tile_cta_acc") return c->cacc ? 1 : 0;
   if (k == "panel_kp") return c->panel_kp;
   if (k == "panel_cols") return c->panel_kd;
