@@ -39,9 +39,13 @@ struct EngineCfg {
   double* hist;       // nullable, max_iters + 1
 };
 
-#define QPK_TILE_DOUBLES 4096     // a dense tile holds <= 4096 values (32 KB)
+#ifndef QPK_TILE_DOUBLES
+#define QPK_TILE_DOUBLES 3072     // a dense tile holds <= 3072 values (24 KB)
+#endif
 #define QPK_TILE_ROWS 64
-#define QPK_TILE_DMAX 1024        // distinct columns per tile
+#ifndef QPK_TILE_DMAX
+#define QPK_TILE_DMAX 512         // distinct columns per tile
+#endif
 
 // Dense row tiles (the "dictionary" mode): tile t covers rows [ra, rb) of B
 // and its ndp (multiple of 4) distinct columns cols[d0 .. d0+ndp) (-1 pads);

@@ -66,7 +66,9 @@ __device__ __forceinline__ uint32_t round_up16(uint32_t b) { return b == 0u ? 16
 //   rows:    t_r = A_r . u_dict  (warp per row), z_r, y_B, fused bottom update
 //   columns: bpart[c] = sum_r A[r][c] z_r  (thread per column, no atomics)
 #define QPK_TILE_WARPS 8
-#define QPK_TILE_STAGES 4
+#ifndef QPK_TILE_STAGES
+#define QPK_TILE_STAGES 6        // ring stages (3 groups consume, 3 in flight)
+#endif
 
 struct alignas(16) DTileStage {
   double a[QPK_TILE_DOUBLES + 2];
@@ -81,11 +83,15 @@ struct alignas(16) DTileStage {
 };
 
 #ifndef QPK_TILE_GROUPS
-#define QPK_TILE_GROUPS 2        // consumer groups working on alternate tiles
+#define QPK_TILE_GROUPS 3        // consumer groups working on tiles round robin
 #endif
+#ifndef QPK_TILE_GWARPS
 #define QPK_TILE_GWARPS 4        // warps per consumer group
+#endif
 #define QPK_TILE_GATHER_WARPS 2  // warps gathering u[cols] for landed tiles
-#define QPK_TILE_UMAX 1536       // CTA-accumulator capacity (distinct columns of a CTA's tiles)
+#ifndef QPK_TILE_UMAX
+#define QPK_TILE_UMAX 1024       // CTA-accumulator capacity (distinct columns of a CTA's tiles)
+#endif
 
 struct DTileSmem {
   DTileStage st[QPK_TILE_STAGES];
@@ -103,8 +109,10 @@ __device__ __forceinline__ void tile_group_bar(int g) {
 // Tile layout: rows of the dense block have an odd pitch (ndp | 1 doubles,
 // TileDescD::pad0) so that 32 lanes reading one column of consecutive rows
 // hit distinct banks.  QPK_TILE_GROUPS groups of QPK_TILE_GWARPS consumer
-// warps take alternate tiles (so one group's barrier-separated passes overlap
-// another's); per tile a group runs three regular shared-memory passes: row
+// warps take the tiles round robin (so the groups' barrier-separated passes
+// overlap: with 3 groups and 6 stages, 3 tiles are in flight while 3 are
+// consumed -- measured best of 2-4 groups x 2-7 stages x 16-32 KB tiles on
+// cfg3/cfg4); per tile a group runs three regular shared-memory passes: row
 // slices (warp w, lane = row), row finish (thread per row), columns (thread
 // per column).
 __global__ void __launch_bounds__((QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32, 1)
