@@ -1,14 +1,17 @@
 """Benchmark: Jacobi-PCG iterations/s on the doubly augmented KKT system.
 
-Workload (BASELINE.json configs[4], "cfg5"): the isolated PCG operator sweep
--- random CSR A 4,000,000 x 1,000,000 with 16 nnz/row (fp64), H =
-diag(U(1e-2,1)), W with log10 w ~ U(-6,6), a fixed 500 Jacobi-PCG iterations
-from a random right-hand side (x0 = 0).  It is the configuration the metric
-"PCG iterations/s and achieved HBM GB/s" is quoted on and the largest one whose
-headline is the PCG sweep; see DESIGN.md section "Measurement".
-
-One step = one direction solve = one call of the hot path: Jacobi build +
-500 PCG iterations + the final true-residual apply (linalg.py:132-133).
+Default workload (BASELINE.json configs[3], "cfg4"): the scaled
+radiation-therapy-like QP -- 2,000,000 voxels x 100,000 beamlets, 0.1 % band
+density (B = -D_oar: 1.6e8 nnz, fp64), H = D_t'D_t (4.1e6 nnz) -- the largest
+configuration of BASELINE.json, the one it names for row sharding over
+1/2/4/8 GPUs and the one the north star's targets (>= 70 % of HBM bandwidth on
+1 GPU, >= 60 % efficiency at 8 GPUs on the largest sharded config) are stated
+on.  The operator is that of the first IPM iteration; one step = one direction
+solve = one call of the hot path: new diagonals (Jacobi rebuilt) + 200 PCG
+iterations from a seeded N(0,1) right-hand side (x0 = 0) + the final
+true-residual apply (linalg.py:132-133).  `--workload cfg1|cfg2|cfg3|cfg5`
+runs the other BASELINE configs the same way (cfg5 = the isolated operator
+sweep, 500 iterations); `--ipm` reports IPM wall time.  See DESIGN.md §5.
 
   value  PCG iterations/s, whole job, inputs resident in HBM
          (qpk_pcg_dev on device buffers), CUDA events on the solver's stream
@@ -35,7 +38,8 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-METRIC = "Jacobi-PCG iterations/s on the doubly augmented KKT system (cfg5 operator sweep)"
+METRIC = "Jacobi-PCG iterations/s on the doubly augmented KKT system"
+CONFIG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
 UNIT = "PCG iterations/s"
 
 
@@ -52,8 +56,9 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=10, help="oracle iterations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters-per-step", type=int, default=5)
-    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
-                    help="cfg5 = headline sweep; cfg1-4 = PCG sweep on the first IPM iteration's operator")
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="cfg4 = headline (largest, sharded config); cfg1-4: PCG sweep on the first IPM iteration's "
+                         "operator; cfg5: the isolated operator sweep")
     ap.add_argument("--ipm", action="store_true",
                     help="IPM wall time of the device-resident IPM on --workload (cfg1 pinned at mu_tol 1e-8, "
                          "CG tol 1e-10; others at the reference defaults)")
@@ -336,12 +341,21 @@ def run_ours(args):
                 traffic_src = rec.get("source")
         except Exception:
             traffic = None
+    # the pass over B (dominant kernel of a PCG iteration): matrix bytes / its time
+    phases = np.mean(phase_ms, axis=0) * 1e3 / args.iters          # us per iteration
+    rows_kernel = {3: "k_slot_rows_tile", 4: "k_slot_panel"}.get(gk.ctx.query("scatter"), "k_slot_rows") \
+        if engine_used else "pcg_kernel (rows phase)"
+    mat_bytes = per_iter - 88 * op.dim
+    dom = {"name": rows_kernel, "us_per_iter": round(float(phases[1]), 2),
+           "share_of_iteration": round(float(phases[1] / max(phases.sum(), 1e-9)), 3),
+           "matrix_bytes_per_iter": mat_bytes,
+           "achieved_matrix_GBs": round(mat_bytes / world / (phases[1] * 1e-6) / 1e9, 1) if phases[1] > 0 else None}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded generator of BASELINE.json configs[4]; no dataset involved)",
+            "data": f"synthetic (seeded generator of BASELINE.json configs[{CONFIG_INDEX[args.workload]}]; no dataset involved)",
             "config": {"workload": WORKLOAD_DESC[args.workload] + (f" (scale {args.scale})" if args.scale != 1 else "")
                                    + f"; {args.iters} PCG iterations per step (+ Jacobi build + final apply)",
                        "parallelism": f"rowshard{world} (NCCL all-reduce per iteration)" if world > 1 else "single",
@@ -358,8 +372,12 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": per_launch, "algorithmic_bytes_per_iter": per_iter,
-                         "kernel": ("slot engine kernels k_slot_top/rows/update (whole solve)" if engine_used else
-                                    f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if gk.ctx.query('scatter') == 2 else 'false'}>"),
+                         "kernel": (f"slot engine: {rows_kernel} + top / combine / update kernels per iteration "
+                                    "(achieved = the whole solve's algorithmic bytes / its device time)"
+                                    if engine_used else
+                                    f"pcg_kernel<{gk.ctx.query('lanes')},{'true' if gk.ctx.query('scatter') == 2 else 'false'}>"
+                                    " (one launch = the whole solve)"),
+                         "dominant_kernel": dom,
                          "kernel_ms_avg": avg_ms,
                          "phase_us_per_iter": dict(zip(["direction_top", "rows_B_Bt", "residual_update",
                                                         "combine_Bt_partials" if engine_used else "other"],
