@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="cfg4 = headline (largest, sharded config); cfg1-4: PCG sweep on the first IPM iteration's "
                          "operator; cfg5: the isolated operator sweep")
+    ap.add_argument("--force-sharded", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--ipm", action="store_true",
                     help="IPM wall time of the device-resident IPM on --workload (cfg1 pinned at mu_tol 1e-8, "
                          "CG tol 1e-10; others at the reference defaults)")
@@ -230,7 +231,7 @@ def run_reference(args):
 def run_ours(args):
     import torch
     rank, world, local = dist_env()
-    if world > 1:
+    if world > 1 or args.force_sharded:
         import torch.distributed as dist
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
@@ -238,7 +239,9 @@ def run_ours(args):
     from paper_2308_00637_b200.direction import GpuKkt, gpu_direction, operator_for
     from paper_2308_00637_b200.pcg import PcgConfig
 
-    sharded_run = world > 1
+    # N > 1: row-sharded; --force-sharded runs the same code path at N = 1
+    # (one-rank NCCL communicator) to validate it on a single GPU
+    sharded_run = world > 1 or args.force_sharded
     # N > 1: every rank builds the same system and owns a row shard of it
     # (strong scaling); N = 1: the whole system on one GPU
     problem, op, rhs, meta = make_workload(args.workload, args.scale, seed_offset=0)
@@ -392,7 +395,7 @@ def run_ours(args):
             line["cpu_baseline"] = cpu_baseline(op, rhs, args.cpu_iters, args.workload)
         print(json.dumps(line), flush=True)
     gk.close()
-    if world > 1:
+    if world > 1 or args.force_sharded:
         torch.distributed.destroy_process_group()
 
 
