@@ -505,7 +505,7 @@ struct qpk_ctx {
   int tile_grid = 0;
   DBuf<int> tile_beg, cta_off, tslot, col_ptr2, col_pos2, comb_beg2, comb_col2;
   DBuf<double> cpart;
-  int comb_lanes2 = 8, comb_nseg2 = 0;
+  int comb_lanes2 = 8, comb_nseg2 = 0, comb_max2 = 0;   // max CTA partials of one column
   DBuf<double> tval;
   DBuf<int4> rtile_desc;
   int n_rtiles = 0;
@@ -1086,6 +1086,8 @@ static int build_dict(qpk_ctx* c) {
       for (long long j = 0; j < n; ++j) cp2[j + 1] += cp2[j];
       std::vector<int> at(cp2.begin(), cp2.end() - 1);
       for (int q = 0; q < off[G]; ++q) cpos2[at[ucols[q]]++] = q;
+      c->comb_max2 = 0;
+      for (long long j = 0; j < n; ++j) c->comb_max2 = std::max(c->comb_max2, cp2[j + 1] - cp2[j]);
       std::vector<int> cseg(n + 1, 0), cbeg;
       for (long long j = 0; j < n; ++j) {
         cseg[j] = (int)cbeg.size();
@@ -1635,6 +1637,9 @@ static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const
   k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
 }
 
+// CTA-accumulation mode with few partials per column: one combine launch
+static bool comb_direct(const qpk_ctx* c) { return c->scatter == QPK_SCATTER_DICT && c->cacc && c->comb_max2 <= 16; }
+
 // does the slot finish B'z with a CSC gather pass (k_slot_csc + seg sums)?
 static bool slot_csc(const qpk_ctx* c) {
   return c->scatter == QPK_SCATTER_CSC || (c->scatter == QPK_SCATTER_PANEL && !c->panel_direct);
@@ -1642,7 +1647,7 @@ static bool slot_csc(const qpk_ctx* c) {
 
 static int slot_launches(const qpk_ctx* c) {
   int k = 2;                                                    // top, update
-  if (c->scatter == QPK_SCATTER_DICT) k += 3 + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
+  if (c->scatter == QPK_SCATTER_DICT) k += (comb_direct(c) ? 2 : 3) + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
   else if (c->scatter == QPK_SCATTER_PANEL) k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0);
   else k += 1 + (slot_csc(c) ? 1 : 0);
   if (c->sharded) k += 2;
@@ -1666,8 +1671,13 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
   } else if (c->scatter == QPK_SCATTER_DICT) {
     k_slot_rows_tile<<<E.G_rows, (QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32,
                        tile_smem(), s>>>(E, par);
-    k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, par);               // y_top += B'z (tile partials)
-    k_comb_col<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);
+    if (comb_direct(c)) {                                      // y_top += B'z (CTA partials)
+      k_comb_direct<<<std::max(1, std::min(G, (int)((c->n + QPK_BLOCK - 1) / QPK_BLOCK))), QPK_BLOCK, 0, s>>>(
+          E, c->y.p, 1, par);
+    } else {
+      k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, par);             // y_top += B'z (tile partials)
+      k_comb_col<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);
+    }
     if (c->hkind != QPK_HESS_DIAG && !c->h_tiled) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
   } else {
     switch (c->lanes * 2 + (csc ? 1 : 0)) {

@@ -410,6 +410,20 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_comb_col(Engine E, double* out, i
   }
 }
 
+// Single-level combine for the CTA-accumulation mode, where a column has only
+// a few CTA partials (banded B: the CTAs whose tile range meets the column's
+// band): out[j] (+)= sum of column j's partials in CTA order, thread per column.
+__global__ void __launch_bounds__(QPK_BLOCK) k_comb_direct(Engine E, double* out, int add, int par) {
+  if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
+  if (par >= 0 && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_mid = globaltimer_ns();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x) {
+    const int b = __ldg(E.dict.col_ptr + j), e = __ldg(E.dict.col_ptr + j + 1);
+    double sum = 0.0;
+    for (int q = b; q < e; ++q) sum += E.dict.cpart[__ldg(E.dict.col_pos + q)];
+    out[j] = add ? out[j] + sum : sum;
+  }
+}
+
 // Jacobi through the tiles: bpart[c] = sum_r A[r][c]^2 / d_r (once per IPM iteration)
 __global__ void __launch_bounds__(QPK_BLOCK) k_jac_tile(Engine E) {
   const Dict& D = E.dict;
