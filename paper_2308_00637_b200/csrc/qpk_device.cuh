@@ -91,6 +91,34 @@ __device__ __forceinline__ double grid_total(const double* part, int G, double* 
   return block_sum(s, red);
 }
 
+// Two slot totals in one pass (one block reduction instead of two; each total
+// keeps the fixed order of grid_total, so results are bitwise those of two
+// grid_total calls).
+__device__ __forceinline__ void grid_total2(const double* pa, int ga, const double* pb, int gb, double* red,
+                                            double& ta, double& tb) {
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < ga; i += blockDim.x) a += pa[i];
+  for (int i = threadIdx.x; i < gb; i += blockDim.x) b += pb[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) { red[warp] = a; red[16 + warp] = b; }
+  __syncthreads();
+  a = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+  b = (lane < (int)(blockDim.x >> 5)) ? red[16 + lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  ta = a;
+  tb = b;
+}
+
 template <int L>
 __device__ __forceinline__ double subwarp_sum(double s) {
 #pragma unroll

@@ -447,9 +447,14 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       pap = E.gscal[0] + E.gscal[1];
       if (c.mode == MODE_RESTART) rz = E.gscal[2] + E.gscal[3];
     } else {
-      pap = grid_total(E.part + SLOT_ROWS * G, E.G_rows, red) + grid_total(E.part + SLOT_PREP * G, G, red);
-      if (c.mode == MODE_RESTART)
-        rz = grid_total(E.part + SLOT_AUX * G, G, red) + grid_total(E.part + SLOT_AUX2 * G, E.G_rows, red);
+      double t_rows, t_prep;
+      grid_total2(E.part + SLOT_ROWS * G, E.G_rows, E.part + SLOT_PREP * G, G, red, t_rows, t_prep);
+      pap = t_rows + t_prep;
+      if (c.mode == MODE_RESTART) {
+        double t_aux, t_aux2;
+        grid_total2(E.part + SLOT_AUX * G, G, E.part + SLOT_AUX2 * G, E.G_rows, red, t_aux, t_aux2);
+        rz = t_aux + t_aux2;
+      }
     }
     if (pap <= 0.0) {                                                   // linalg.py:102-103
       if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -518,8 +523,8 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
   if (!last_block(E.counter)) return;
 
   // ---- decision (one block) ----
-  const double rr_tot = grid_total(E.part + SLOT_RR * G, G, red);
-  const double rz_tot = grid_total(E.part + SLOT_RZ * G, G, red);
+  double rr_tot, rz_tot;
+  grid_total2(E.part + SLOT_RR * G, G, E.part + SLOT_RZ * G, G, red, rr_tot, rz_tot);
   if (threadIdx.x != 0) return;
   if (E.sharded) {
     // rank-local totals; summed over ranks by the collective, then k_slot_decide
