@@ -39,8 +39,10 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "Jacobi-PCG iterations/s on the doubly augmented KKT system"
-CONFIG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4}
+CONFIG_INDEX = {"cfg1": 0, "cfg2": 1, "cfg3": 2, "cfg4": 3, "cfg5": 4, "svm_dual": 1}
 UNIT = "PCG iterations/s"
+L2_GATHER_PER_S = 287e9      # random 8 B gathers from an L2-resident table (measured)
+L2_ATOMIC_PER_S = 190e9      # random fp64 atomics into an L2-resident table (measured)
 
 
 def parse():
@@ -56,7 +58,7 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=10, help="oracle iterations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-iters-per-step", type=int, default=5)
-    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+    ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "svm_dual"],
                     help="cfg4 = headline (largest, sharded config); cfg1-4: PCG sweep on the first IPM iteration's "
                          "operator; cfg5: the isolated operator sweep")
     ap.add_argument("--force-sharded", action="store_true", help=argparse.SUPPRESS)
@@ -83,6 +85,8 @@ WORKLOAD_DESC = {
     "cfg2": "cfg2 SVM primal d=500, N=50,000 (A = [diag(y)X, y, I], 502 nnz/row)",
     "cfg3": "cfg3 RT-like 200,000 voxels x 20,000 beamlets, 0.5% band density, SparseHessian D_t'D_t",
     "cfg4": "cfg4 RT-like 2,000,000 voxels x 100,000 beamlets, 0.1% band density, SparseHessian D_t'D_t",
+    "svm_dual": "kernel-SVM dual (svm.py:179-195) at the dense-kernel cap: n=20,000 samples, d=100, RBF sigma=100, "
+                "C=1; H = (y y') * K built on the device (3.2 GB dense), one equality row",
     "cfg5": "cfg5 operator sweep 4,000,000 x 1,000,000, 16 nnz/row, H=diag(U(1e-2,1)), log10 w ~ U(-6,6)",
 }
 
@@ -92,7 +96,16 @@ def make_workload(name: str, scale: float, seed_offset: int = 0):
     cfg1-4: the operator of the first IPM iteration with a seeded N(0,1) rhs."""
     from paper_2308_00637_b200 import workloads
     from paper_2308_00637_b200.problem import build_operator
-    if name == "cfg5":
+    if name == "svm_dual":
+        from paper_2308_00637_b200 import svm
+        from paper_2308_00637_b200.workloads import _state_from_initial
+        x, y = workloads.svm_dual_data(seed=6 + seed_offset, n=int(20_000 * scale), d=100)
+        data = svm.SvmDataset.from_dense(x, y)
+        problem = svm.build_svm_dual(data, svm.SvmConfig(sigma=100.0, c=1.0))
+        state = _state_from_initial(problem)
+        meta = {"seed": 6 + seed_offset, "n": len(y), "d": 100, "x": x, "y": y, "sigma": 100.0, "c": 1.0}
+        rhs = np.random.default_rng(77 + seed_offset).standard_normal(problem.n + 1)
+    elif name == "cfg5":
         m, n = int(4_000_000 * scale), int(1_000_000 * scale)
         problem, state, meta = workloads.random_sweep(seed=5 + seed_offset, m=m, n=n)
         rhs = meta.pop("rhs")
@@ -111,6 +124,8 @@ def make_workload(name: str, scale: float, seed_offset: int = 0):
                                                                       + problem.m_eq)
     op = build_operator(problem, state)
     assert len(rhs) == op.dim
+    if name == "svm_dual":
+        _SVM_META.update(meta)
     return problem, op, rhs, meta
 
 
@@ -130,7 +145,7 @@ def algorithmic_bytes(op, iters: int, applies: int):
     kind = type(h).__name__
     if kind == "SparseHessian":
         bytes_h = 12 * h.m.nnz + 4 * (p.n + 1)
-    elif kind == "DenseHessian":
+    elif kind in ("DenseHessian", "DeviceDenseHessian"):
         bytes_h = 8 * p.n * p.n
     elif kind == "QuasiNewtonHessian":
         bytes_h = 16 * p.n * h.u.shape[1] + 8 * h.u.shape[1]
@@ -184,10 +199,27 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def host_operator(op, meta=None):
+    """The oracle needs host data: the SVM dual's device Hessian is rebuilt on
+    the host by the oracle's restatement of _gram_matrix (not timed)."""
+    if type(op.problem.hessian).__name__ != "DeviceDenseHessian":
+        return op
+    from oracle import svm_oracle as so
+    from paper_2308_00637_b200.problem import build_operator
+    from paper_2308_00637_b200.workloads import _state_from_initial
+    meta = meta or _SVM_META
+    prob = so.dual_problem(meta["x"], meta["y"], meta["sigma"], meta["c"])
+    return build_operator(prob, _state_from_initial(prob))
+
+
+_SVM_META = {}
+
+
 def cpu_baseline(op, rhs, iters: int, name: str = "cfg5"):
     """The reference path (oracle restatement, bit-identical to qpipm on the
     golden vectors) on a bounded sample: `iters` PCG iterations of cfg5."""
     from oracle import qp_oracle as orc
+    op = host_operator(op)
     orc.jacobi_diagonal(op)              # warm the scipy views (not timed)
     t0 = time.perf_counter()
     res = orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=iters))
@@ -203,7 +235,17 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    problem, op, rhs, meta = make_workload(args.workload, args.scale)
+    if args.workload == "svm_dual":
+        from paper_2308_00637_b200.problem import build_operator
+        from paper_2308_00637_b200.workloads import _state_from_initial, svm_dual_data
+        from oracle import svm_oracle as so
+        x, y = svm_dual_data(seed=6, n=int(20_000 * args.scale), d=100)
+        problem = so.dual_problem(x, y, 100.0, 1.0)
+        op = build_operator(problem, _state_from_initial(problem))
+        rhs = np.random.default_rng(77).standard_normal(op.dim)
+        meta = {"seed": 6}
+    else:
+        problem, op, rhs, meta = make_workload(args.workload, args.scale)
     from oracle import qp_oracle as orc
     k_iter = args.ref_iters_per_step
     orc.jacobi_diagonal(op)
@@ -391,6 +433,19 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
+        if gk.ctx.query("scatter") == 1 and phases[1] > 0:
+            # random B (cfg5): each nonzero costs one random u gather and one
+            # random fp64 atomic in L2; their measured ceilings on B200
+            # (probes/random_probe.cu, profiles/r01_probe_random_access2.txt)
+            # bound the rows phase before HBM does
+            nnz = gk.ctx.query("nnz") / world
+            floor_us = (nnz / L2_GATHER_PER_S + nnz / L2_ATOMIC_PER_S) * 1e6
+            line["roofline"]["l2_request_bound"] = {
+                "gathers_per_iter": nnz, "atomics_per_iter": nnz,
+                "gather_rate_per_s": L2_GATHER_PER_S, "atomic_rate_per_s": L2_ATOMIC_PER_S,
+                "floor_us_per_iter": round(floor_us, 1), "rows_phase_us_per_iter": round(float(phases[1]), 1),
+                "frac": round(floor_us / float(phases[1]), 3),
+                "source": "profiles/r01_probe_random_access2.txt (8 MB table, 148 SMs)"}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(op, rhs, args.cpu_iters, args.workload)
         print(json.dumps(line), flush=True)
@@ -412,6 +467,8 @@ def ipm_problem(name):
         problem, _, _ = workloads.rt_like(seed=3)
     elif name == "cfg4":
         problem, _, _ = workloads.rt_like(seed=4, n_vox=2_000_000, n_beam=100_000, density=0.001)
+    elif name == "svm_dual":
+        problem, _, _, _ = make_workload("svm_dual", 1.0)
     else:
         raise SystemExit("--ipm needs --workload cfg1..cfg4 (cfg5 is a fixed-iteration PCG sweep)")
     return problem, IpmConfig()
@@ -459,6 +516,9 @@ def run_ipm(args):
         k = args.cpu_ipm_iters or (cfg.max_iters if args.workload == "cfg1" else 2)
         ocfg = orc.IpmConfig(gamma=cfg.gamma, mu_init=cfg.mu_init, mu_tol=cfg.mu_tol, mu_shrink=cfg.mu_shrink,
                              max_iters=k, pcg=orc.PcgConfig(tol=cfg.pcg.tol, max_iters=cfg.pcg.max_iters))
+        if args.workload == "svm_dual":            # the oracle needs the Hessian on the host
+            from oracle import svm_oracle as so
+            problem = so.dual_problem(_SVM_META["x"], _SVM_META["y"], _SVM_META["sigma"], _SVM_META["c"])
         orep = orc.solve(problem, ocfg)
         full = orep.status == "converged"
         line["cpu_baseline"] = {

@@ -130,6 +130,25 @@ int qpk_set_hessian_csr(qpk_ctx* ctx, const int64_t* row_offsets, const int64_t*
 int qpk_set_hessian_dense(qpk_ctx* ctx, const double* m_rowmajor);
 int qpk_set_hessian_lowrank(qpk_ctx* ctx, const double* h0, int64_t k, const double* u_rowmajor,
                             const double* w);
+/* dense H from a DEVICE matrix (n x n row-major, copied at finalize): the SVM
+ * dual's Gram-based Hessian never leaves the GPU */
+int qpk_set_hessian_dense_dev(qpk_ctx* ctx, const double* m_rowmajor_dev);
+
+/* ---- SVM dual frontend ----------------------------
+ * H[i][j] = y_i y_j exp(-max(|x_i|^2 + |x_j|^2 - 2 x_i.x_j, 0) / (2 sigma)),
+ * exactly symmetric: the Hessian build_svm_dual makes from _gram_matrix
+ * (qpipm/svm.py:166-176, 185).  X (n x d row-major), y (n), H (n x n
+ * row-major): device pointers; runs on the context's stream.  Usable before
+ * or without a problem. */
+int qpk_rbf_hessian_dev(qpk_ctx* ctx, const double* X, int64_t n, int64_t d, const double* y, double sigma,
+                        double* H);
+/* out = H v with the finalized problem's Hessian (hessian_apply, model.py:165-176,
+ * without q_extra); dense and diagonal H.  Device pointers. */
+int qpk_hessian_apply_dev(qpk_ctx* ctx, const double* v, double* out);
+/* out = M v for a dense n x n row-major DEVICE matrix (the SVM decision values
+ * g = y o (H alpha), svm.py:194-196, with the Hessian already on the device) */
+int qpk_dense_gemv_dev(qpk_ctx* ctx, const double* m_rowmajor_dev, int64_t n, const double* v, double* out);
+
 /* builds the device layout; scatter = QPK_SCATTER_* */
 int qpk_problem_finalize(qpk_ctx* ctx, int scatter);
 

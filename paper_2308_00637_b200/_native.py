@@ -28,6 +28,7 @@ EXPORTED = (
     "qpk_problem_finalize", "qpk_set_diagonals", "qpk_set_diagonals_dev", "qpk_jacobi",
     "qpk_apply", "qpk_apply_dev", "qpk_pcg", "qpk_pcg_dev", "qpk_query",
     "qpk_nccl_get_unique_id", "qpk_shard_init", "qpk_ipm_set_bounds", "qpk_ipm_solve",
+    "qpk_set_hessian_dense_dev", "qpk_rbf_hessian_dev", "qpk_hessian_apply_dev", "qpk_dense_gemv_dev",
 )
 
 
@@ -87,6 +88,10 @@ _SIGS = {
     "qpk_set_hessian_csr": ([_P, _P, _P, _P], _I),
     "qpk_set_hessian_dense": ([_P, _P], _I),
     "qpk_set_hessian_lowrank": ([_P, _P, _I64, _P, _P], _I),
+    "qpk_set_hessian_dense_dev": ([_P, _P], _I),
+    "qpk_rbf_hessian_dev": ([_P, _P, _I64, _I64, _P, _D, _P], _I),
+    "qpk_hessian_apply_dev": ([_P, _P, _P], _I),
+    "qpk_dense_gemv_dev": ([_P, _P, _I64, _P, _P], _I),
     "qpk_problem_finalize": ([_P, _I], _I),
     "qpk_set_diagonals": ([_P, _P, _P], _I),
     "qpk_set_diagonals_dev": ([_P, _P, _P], _I),

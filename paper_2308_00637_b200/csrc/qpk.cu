@@ -30,6 +30,7 @@
 #include "qpk_panel.cuh"
 #include "qpk_cluster.cuh"
 #include "qpk_ipm.cuh"
+#include "qpk_svm.cuh"
 #include <chrono>
 
 namespace cg = cooperative_groups;
@@ -486,6 +487,7 @@ struct qpk_ctx {
   std::vector<double> h_h;               // diag d / low-rank h0
   std::vector<int> h_hrp, h_hci; std::vector<double> h_hv;
   std::vector<double> h_dense, h_U, h_w;
+  const double* h_dense_dev = nullptr;  // dense H given as a device matrix (copied at finalize)
 
   int scatter = QPK_SCATTER_ATOMIC;
   int lanes = 4, csc_lanes = 8, h_lanes = 8;
@@ -821,6 +823,32 @@ int qpk_set_hessian_dense(qpk_ctx* c, const double* mm) {
   if (!c || !c->building || !mm) return fail(QPK_E_STATE, "qpk_set_hessian_dense: bad state/arg");
   c->hkind = QPK_HESS_DENSE;
   c->h_dense.assign(mm, mm + c->n * c->n);
+  return QPK_OK;
+}
+
+int qpk_set_hessian_dense_dev(qpk_ctx* c, const double* mm) {
+  if (!c || !c->building || !mm) return fail(QPK_E_STATE, "qpk_set_hessian_dense_dev: bad state/arg");
+  c->hkind = QPK_HESS_DENSE;
+  std::vector<double>().swap(c->h_dense);
+  c->h_dense_dev = mm;
+  return QPK_OK;
+}
+
+int qpk_rbf_hessian_dev(qpk_ctx* c, const double* X, int64_t n, int64_t d, const double* y, double sigma,
+                        double* H) {
+  if (!c || !X || !y || !H || n < 1 || d < 0) return fail(QPK_E_ARG, "qpk_rbf_hessian_dev: bad argument");
+  if (!(sigma > 0.0)) return fail(QPK_E_ARG, "qpk_rbf_hessian_dev: sigma must be positive");
+  if ((n + QPK_GRAM_T - 1) / QPK_GRAM_T > 65535) return fail(QPK_E_ARG, "qpk_rbf_hessian_dev: n too large");
+  CUDA_TRY(cudaSetDevice(c->device));
+  cudaStream_t s = c->stream;
+  double* sq = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&sq, n * sizeof(double), s));
+  k_rowsq<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(X, n, d, sq);
+  const unsigned T = (unsigned)((n + QPK_GRAM_T - 1) / QPK_GRAM_T);
+  k_rbf_hessian<<<dim3(T, T), 256, 0, s>>>(X, n, d, y, sq, 1.0 / (2.0 * sigma), H);
+  c->launches += 2;
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaFreeAsync(sq, s));
   return QPK_OK;
 }
 
@@ -1229,6 +1257,7 @@ static int build_cluster(qpk_ctx* c) {
   if (getenv("QPK_NO_CLUSTER") || c->sharded || c->hkind == QPK_HESS_LOWRANK) return QPK_OK;
   const long long n = c->n, m = c->m;
   if (n > 16384 || (long long)c->h_ci.size() > 4000000) return QPK_OK;
+  if (c->hkind == QPK_HESS_DENSE && c->h_dense.size() != (size_t)(n * n)) return QPK_OK;   // device-given H
   // H as full CSR rows
   std::vector<int> hrp(n + 1, 0), hci;
   std::vector<double> hv;
@@ -1357,7 +1386,14 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     CUDA_TRY(upload(c->hci, c->h_hci, s));
     CUDA_TRY(upload(c->hv, c->h_hv, s));
   }
-  if (c->hkind == QPK_HESS_DENSE) CUDA_TRY(upload(c->hdense, c->h_dense, s));
+  if (c->hkind == QPK_HESS_DENSE && c->h_dense_dev) {
+    CUDA_TRY(c->hdense.alloc((size_t)c->n * c->n));
+    CUDA_TRY(cudaMemcpyAsync(c->hdense.p, c->h_dense_dev, (size_t)c->n * c->n * sizeof(double),
+                             cudaMemcpyDeviceToDevice, s));
+    c->h_dense_dev = nullptr;
+  } else if (c->hkind == QPK_HESS_DENSE) {
+    CUDA_TRY(upload(c->hdense, c->h_dense, s));
+  }
   if (c->hkind == QPK_HESS_LOWRANK) {
     CUDA_TRY(upload(c->U, c->h_U, s));
     CUDA_TRY(upload(c->w, c->h_w, s));
@@ -1601,6 +1637,38 @@ int qpk_apply(qpk_ctx* c, const double* v, double* y) {
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(y, c->y.p, bytes, cudaMemcpyDeviceToHost, c->stream));
   CUDA_TRY(cudaStreamSynchronize(c->stream));
+  return QPK_OK;
+}
+
+// out = H v with the problem's Hessian (hessian_apply, model.py:165-176,
+// without q_extra); dense and diagonal H
+__global__ void k_diag_mul(const double* h, const double* v, double* out, long long n) {
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x)
+    out[j] = h[j] * v[j];
+}
+
+int qpk_hessian_apply_dev(qpk_ctx* c, const double* v, double* out) {
+  if (!c || !c->finalized) return fail(QPK_E_STATE, "qpk_hessian_apply_dev: problem not finalized");
+  if (!v || !out) return fail(QPK_E_ARG, "qpk_hessian_apply_dev: null vector");
+  CUDA_TRY(cudaSetDevice(c->device));
+  if (c->hkind == QPK_HESS_DENSE) {
+    k_dense_gemv<<<c->sms * 8, 256, 0, c->stream>>>(c->hdense.p, c->n, v, out);
+  } else if (c->hkind == QPK_HESS_DIAG) {
+    k_diag_mul<<<c->sms * 4, 256, 0, c->stream>>>(c->hh.p, v, out, c->n);
+  } else {
+    return fail(QPK_E_UNSUPPORTED, "qpk_hessian_apply_dev: dense and diagonal Hessians only");
+  }
+  c->launches++;
+  CUDA_TRY(cudaGetLastError());
+  return QPK_OK;
+}
+
+int qpk_dense_gemv_dev(qpk_ctx* c, const double* Hm, int64_t n, const double* v, double* out) {
+  if (!c || !Hm || !v || !out || n < 1) return fail(QPK_E_ARG, "qpk_dense_gemv_dev: bad argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  k_dense_gemv<<<c->sms * 8, 256, 0, c->stream>>>(Hm, n, v, out);
+  c->launches++;
+  CUDA_TRY(cudaGetLastError());
   return QPK_OK;
 }
 

@@ -219,7 +219,27 @@ __device__ __forceinline__ double hess_rows(const Op& op, const double* u, doubl
     for (int j = gwarp; j < op.n; j += nwarp) {
       const double* row = op.H.dense + (size_t)j * op.n;
       double s = 0.0;
-      for (int c = ln; c < op.n; c += 32) s = fma(__ldg(row + c), u[c], s);
+      if ((op.n & 1) == 0 && (reinterpret_cast<uintptr_t>(u) & 15) == 0) {
+        // 16-byte loads, four independent chains (SVM dual: H is the whole operator)
+        const double2* r2 = reinterpret_cast<const double2*>(row);
+        const double2* u2 = reinterpret_cast<const double2*>(u);
+        const int h = op.n >> 1;
+        double s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int c = ln;
+        for (; c + 32 < h; c += 64) {
+          const double2 a = __ldg(r2 + c), b = __ldg(r2 + c + 32);
+          const double2 x = u2[c], z = u2[c + 32];
+          s = fma(a.x, x.x, s); s1 = fma(a.y, x.y, s1);
+          s2 = fma(b.x, z.x, s2); s3 = fma(b.y, z.y, s3);
+        }
+        for (; c < h; c += 32) {
+          const double2 a = __ldg(r2 + c), x = u2[c];
+          s = fma(a.x, x.x, s); s1 = fma(a.y, x.y, s1);
+        }
+        s = (s + s1) + (s2 + s3);
+      } else {
+        for (int c = ln; c < op.n; c += 32) s = fma(__ldg(row + c), u[c], s);
+      }
       s = subwarp_sum<32>(s);
       if (ln == 0) { atomicAdd(y + j, s); acc += u[j] * s; }
     }

@@ -77,6 +77,9 @@ class GpuKkt:
             mm = np.ascontiguousarray(h.m, dtype=np.float64)
             _dim(mm.shape[0], self.n, "Hessian")
             c.call("qpk_set_hessian_dense", _native.ptr(mm))
+        elif kind == "DeviceDenseHessian":             # SVM dual: built on the device (svm.py)
+            _dim(h.n, self.n, "Hessian")
+            c.call("qpk_set_hessian_dense_dev", int(h.m_dev.data_ptr()))
         elif kind == "QuasiNewtonHessian":
             h0 = np.ascontiguousarray(h.h0_diag, dtype=np.float64)
             u = np.ascontiguousarray(h.u, dtype=np.float64)

@@ -183,3 +183,19 @@ CONFIGS = {
                                           density=0.001, **kw),
     "cfg5": random_sweep,
 }
+
+
+def svm_dual_data(seed: int = 6, n: int = 20_000, d: int = 100, sep: float = 1.0, noise: float = 0.1):
+    """Samples for the kernel-SVM dual (qpipm/svm.py:179-195): two Gaussian
+    classes with means +-(sep/2)/sqrt(d) * 1, identity covariance, balanced
+    +-1 labels with a fraction `noise` flipped -- the class model of
+    BASELINE.json configs[1], at the dual frontend's dense-kernel cap
+    (MAX_PRECOMPUTED_SAMPLES = 20,000, svm.py:11) by default.
+    Returns (X dense n x d, y)."""
+    rng = np.random.default_rng(seed)
+    y = np.where(rng.permutation(n) < n // 2, 1.0, -1.0)
+    x = rng.standard_normal((n, d)) + y[:, None] * (0.5 * sep / np.sqrt(d))
+    flip = rng.permutation(n)[: int(noise * n)]
+    y = y.copy()
+    y[flip] = -y[flip]
+    return x, y
