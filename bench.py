@@ -433,7 +433,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
-        if gk.ctx.query("scatter") == 1 and phases[1] > 0:
+        if args.workload == "cfg5" and gk.ctx.query("scatter") == 1 and phases[1] > 0:
             # random B (cfg5): each nonzero costs one random u gather and one
             # random fp64 atomic in L2; their measured ceilings on B200
             # (probes/random_probe.cu, profiles/r01_probe_random_access2.txt)

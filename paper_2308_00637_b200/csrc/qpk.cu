@@ -289,7 +289,22 @@ __global__ void __launch_bounds__(QPK_BLOCK, QPK_PCG_MIN_BLOCKS) pcg_kernel(PcgP
 __global__ void __launch_bounds__(QPK_BLOCK) k_hess(Op op, const double* u, double* y, double* part, int G) {
   __shared__ double red[32];
   __shared__ double s_lr[QPK_KMAX];
-  hess_rows(op, u, y, part, G, red, s_lr);
+  if (op.H.kind == HESS_DENSE && op.H.sym) hess_sym(op, u, y);
+  else hess_rows(op, u, y, part, G, red, s_lr);
+}
+
+// dense symmetric H -> its upper 64 x 64 tiles, tile (I, J >= I) at
+// I*nt - I*(I-1)/2 + (J - I), zero padded past n
+__global__ void __launch_bounds__(256) k_pack_sym(const double* __restrict__ Hd, long long n, int nt,
+                                                 double* __restrict__ out) {
+  const int I = blockIdx.y, J = blockIdx.x;
+  if (J < I) return;
+  const size_t t = (size_t)I * nt - (size_t)I * (I - 1) / 2 + (J - I);
+  double* dst = out + t * 4096;
+  for (int e = threadIdx.x; e < 4096; e += 256) {
+    const long long r = (long long)I * 64 + e / 64, col = (long long)J * 64 + e % 64;
+    dst[e] = (r < n && col < n) ? Hd[r * n + col] : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(QPK_BLOCK) k_prep(Op op, const double* v, double* y, double* part, int G) {
@@ -517,6 +532,11 @@ struct qpk_ctx {
   bool have_dict = false, h_tiled = false;
   double dict_reuse = 0.0;        // tile density: nonzeros / dense tile slots
   DBuf<double> bv, cv, hh, hv, hdense, U, w, hdiag;
+  DBuf<double> hsym;             // dense H as packed upper tiles (large dense H)
+  DBuf<double> cdense;           // the leading dense rows of B as dense n-vectors
+  int n_dense = 0;
+  DBuf<int4> hchunks;
+  int h_nchunks = 0;
   bool have_csc = false;
   // dense column panel (QPK_SCATTER_PANEL)
   bool have_panel = false;
@@ -575,8 +595,10 @@ struct qpk_ctx {
     o.cp = cp.p; o.ri = ri.p; o.cv = cv.p; o.csc_lanes = csc_lanes;
     o.H.kind = hkind; o.H.h = hh.p; o.H.rp = hrp.p; o.H.ci = hci.p; o.H.v = hv.p; o.H.lanes = h_lanes;
     o.H.dense = hdense.p; o.H.U = U.p; o.H.w = w.p; o.H.k = (int)hk;
+    o.H.sym = hsym.p; o.H.chunks = hchunks.p; o.H.nchunks = h_nchunks;
     o.d = d.p; o.q = q.p;
     o.top_owner = rank == 0 ? 1 : 0;
+    o.r0 = 0; o.ndense = 0; o.cdense = nullptr;        // dense-row split: slot engine only (make_engine)
     return o;
   }
   long long N() const { return n + m; }
@@ -588,6 +610,14 @@ static cudaError_t upload(DBuf<T>& dst, const std::vector<T>& src, cudaStream_t 
   if (e != cudaSuccess || src.empty()) return e;
   return cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
+
+#ifndef QPK_SYM_MIN_N
+#define QPK_SYM_MIN_N 512      // dense H at least this large is applied from packed symmetric tiles
+#endif
+#define QPK_SYM_CHUNK 2        // tiles per hess_sym work unit
+#ifndef QPK_DENSE_ROW_MIN
+#define QPK_DENSE_ROW_MIN 2048 // a leading B row this long (and >= n/4) is applied as a dense vector
+#endif
 
 static int engine_setup(qpk_ctx* c);
 static Engine make_engine(qpk_ctx* c);
@@ -1495,6 +1525,42 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     int rc = build_cluster(c);
     if (rc) return rc;
   }
+  // large dense H (the SVM dual's Gram Hessian): keep its upper tiles packed,
+  // half the bytes per apply (hess_sym); the row-major copy stays for diag(H)
+  c->h_nchunks = 0;
+  if (c->hkind == QPK_HESS_DENSE && c->cl_C == 0 && !c->sharded && c->n >= QPK_SYM_MIN_N && !getenv("QPK_NO_SYM")) {
+    const int nt = (int)((c->n + 63) / 64);
+    const size_t tiles = (size_t)nt * (nt + 1) / 2;
+    CUDA_TRY(c->hsym.alloc(tiles * 4096));
+    k_pack_sym<<<dim3(nt, nt), 256, 0, s>>>(c->hdense.p, c->n, nt, c->hsym.p);
+    c->launches++;
+    std::vector<int4> ch;
+    for (int I = 0; I < nt; ++I) {
+      const int base = (int)((size_t)I * nt - (size_t)I * (I - 1) / 2);
+      for (int J0 = I; J0 < nt; J0 += QPK_SYM_CHUNK)
+        ch.push_back(make_int4(I, J0, std::min(J0 + QPK_SYM_CHUNK, nt), base + (J0 - I)));
+    }
+    CUDA_TRY(upload(c->hchunks, ch, s));
+    c->h_nchunks = (int)ch.size();
+  }
+  // leading dense rows of B (the SVM dual's y' alpha = 0): as dense vectors,
+  // applied outside the row pass by the slot engine (one warp per row would
+  // serialise n entries)
+  c->n_dense = 0;
+  if (!c->sharded && !getenv("QPK_NO_DENSE_ROWS") &&
+      (c->scatter == QPK_SCATTER_ATOMIC || c->scatter == QPK_SCATTER_CSC)) {
+    const long long thr = std::max<long long>(QPK_DENSE_ROW_MIN, c->n / 4);
+    int k = 0;
+    while (k < QPK_DENSE_ROWS_MAX && k < c->m && c->h_rp[k + 1] - c->h_rp[k] >= thr) ++k;
+    if (k > 0) {
+      std::vector<double> cd((size_t)k * c->n, 0.0);
+      for (int r = 0; r < k; ++r)
+        for (int e = c->h_rp[r]; e < c->h_rp[r + 1]; ++e)
+          if (c->h_ci[e] >= 0) cd[(size_t)r * c->n + c->h_ci[e]] = c->h_v[e];
+      CUDA_TRY(upload(c->cdense, cd, s));
+      c->n_dense = k;
+    }
+  }
   Op o = c->op();
   k_hdiag<<<std::max(1, std::min(c->sms * 4, (int)((c->n + 255) / 256))), 256, 0, s>>>(o.H, (int)c->n, c->hdiag.p);
   c->launches++;
@@ -1623,6 +1689,7 @@ static int apply_impl(qpk_ctx* c, const double* v_dev, double* y_dev) {
   else launch_rows<false>(c->lanes, G, s, o, v_dev, y_dev, c->zb.p, c->part.p, G);
   c->launches += 2;
   if (csc) { k_finish_csc<<<G, QPK_BLOCK, 0, s>>>(o, y_dev, c->zb.p); c->launches++; }
+  if (c->h_nchunks) { k_hess<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev, c->part.p, G); c->launches++; }
   CUDA_TRY(cudaGetLastError());
   return allreduce_sum(c, y_dev, c->n, s);          // sharded: y_top = sum of the ranks' partials
 }
@@ -1717,7 +1784,7 @@ static int slot_launches(const qpk_ctx* c) {
   int k = 2;                                                    // top, update
   if (c->scatter == QPK_SCATTER_DICT) k += (comb_direct(c) ? 2 : 3) + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
   else if (c->scatter == QPK_SCATTER_PANEL) k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0);
-  else k += 1 + (slot_csc(c) ? 1 : 0);
+  else k += 1 + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 1 : 0) + (c->n_dense ? 1 : 0);
   if (c->sharded) k += 2;
   return k;
 }
@@ -1762,7 +1829,13 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
       case 64: launch_slot_rows_t<32, false>(c, G, s, E, par); break;
       default: launch_slot_rows_t<32, true>(c, G, s, E, par); break;
     }
+    if (c->n_dense) {                                                  // dense rows of B, before the CSC gather
+      if (csc) k_slot_dense<true><<<G, QPK_BLOCK, 0, s>>>(E, par);
+      else k_slot_dense<false><<<G, QPK_BLOCK, 0, s>>>(E, par);
+    }
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
+    if (c->h_nchunks)                                                  // packed symmetric dense H
+      k_slot_hess_sym<<<QPK_SYM_MINB * c->sms, QPK_BLOCK, 0, s>>>(E, par);
   }
 }
 
@@ -1831,6 +1904,9 @@ static Engine make_engine(qpk_ctx* c) {
   E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
   E.scatter = c->scatter;
   E.sharded = c->sharded ? 1 : 0;
+  if (c->n_dense && (c->scatter == QPK_SCATTER_ATOMIC || c->scatter == QPK_SCATTER_CSC)) {
+    E.op.r0 = c->n_dense; E.op.ndense = c->n_dense; E.op.cdense = c->cdense.p;
+  }
   E.gscal = c->gscal.p; E.lscal2 = c->lscal2.p; E.abuf = c->abuf.p;
   E.dict.nblk = c->nblk; E.dict.tiles = c->tiles.p; E.dict.cols = c->dcols.p; E.dict.tval = c->tval.p;
   E.dict.bpart = c->bpart.p; E.dict.col_ptr = c->col_ptr.p; E.dict.col_pos = c->col_pos.p;
@@ -1942,8 +2018,9 @@ static int pcg_engine(qpk_ctx* c, double tol, int rel, int64_t max_iters, double
 extern "C" {
 
 static bool use_engine(qpk_ctx* c) {
-  if (c->scatter == QPK_SCATTER_DICT || c->scatter == QPK_SCATTER_PANEL || c->sharded)
-    return true;                                 // tile / panel kernels, collectives: engine only
+  if (c->scatter == QPK_SCATTER_DICT || c->scatter == QPK_SCATTER_PANEL || c->sharded || c->h_nchunks ||
+      c->n_dense)
+    return true;                                 // tile / panel / packed-H kernels, collectives: engine only
   if (c->engine >= 0) return c->engine == 1;
   const char* env = getenv("QPK_ENGINE");
   if (env) return atoi(env) == 1;
@@ -2307,6 +2384,8 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "dict_blocks") return c->nblk;
   if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "hess_tiled") return c->h_tiled ? 1 : 0;
+  if (k == "hess_sym") return c->h_nchunks > 0 ? 1 : 0;
+  if (k == "dense_rows") return c->n_dense;
   if (k == "cluster") return c->cl_C;
   if (k == "tile_cta_acc") return c->cacc ? 1 : 0;
   if (k == "panel_kp") return c->panel_kp;

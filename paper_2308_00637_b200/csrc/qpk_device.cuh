@@ -30,6 +30,9 @@ struct Hess {
   const double* h;                      // DIAG: d ; LOWRANK: h0
   const int* rp; const int* ci; const double* v; int lanes;  // CSR (full symmetric storage)
   const double* dense;                  // n x n row-major
+  const double* sym;                    // dense H as packed upper 64 x 64 tiles (null: not built)
+  const int4* chunks;                   // sym work units {I, J0, J1, tile of (I, J0)}
+  int nchunks;
   const double* U; const double* w; int k;                  // LOWRANK: U n x k row-major
 };
 
@@ -41,11 +44,18 @@ struct Op {
   const double* d;                      // d_diag, m
   const double* q;                      // q_diag_extra, n
   int top_owner;                        // this rank adds the (replicated) top-block terms once
+  // slot engine only: the first ndense rows of B are dense (e.g. the SVM dual's
+  // y' alpha = 0 row, n entries) and are handled as dense vectors outside the
+  // row pass (dot partials in the top kernel, k_slot_dense); r0 = ndense rows
+  // are skipped by phase_rows.  Zero everywhere else.
+  int r0, ndense;
+  const double* cdense;                 // ndense x n row-major
 };
 
 // partial-sum slots (slot-major: part[slot * G + cta])
+#define QPK_DENSE_ROWS_MAX 4
 enum { SLOT_ROWS = 0, SLOT_PREP = 1, SLOT_RR = 2, SLOT_RZ = 3, SLOT_AUX = 4, SLOT_AUX2 = 5, SLOT_S = 6,
-       NSLOTS = SLOT_S + QPK_KMAX };
+       SLOT_DR = SLOT_S + QPK_KMAX, NSLOTS = SLOT_DR + QPK_DENSE_ROWS_MAX };
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
@@ -214,6 +224,8 @@ __device__ __forceinline__ double hess_rows(const Op& op, const double* u, doubl
       for (int o = LH / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       if (j < op.n && lh == 0) { atomicAdd(y + j, s); acc += u[j] * s; }
     }
+  } else if (kind == HESS_DENSE && op.H.sym) {
+    return 0.0;                                        // packed symmetric tiles: hess_sym (own launch)
   } else if (kind == HESS_DENSE) {
     const int ln = threadIdx.x & 31;
     for (int j = gwarp; j < op.n; j += nwarp) {
@@ -266,6 +278,86 @@ __device__ __forceinline__ double hess_rows(const Op& op, const double* u, doubl
   return acc;
 }
 
+// H u for a dense SYMMETRIC H stored as its upper 64 x 64 tiles (half the
+// bytes of the row-major matrix).  One warp per work unit (a run of <= 2 tiles
+// of one tile row I): lane l holds columns 2l, 2l+1 of each 512-byte tile row
+// (one coalesced 16-byte load per lane per row, 32 in flight), so
+//   columns:  (H_IJ' u_I)_c accumulates in registers  -> y_J  (J != I)
+//   rows:     (H_IJ u_J)_r needs a sum over lanes: 32 rows at a time, a
+//             transposed butterfly (31 shuffles) leaves row r0+l in lane l;
+//             accumulated over the unit's tiles -> y_I
+// Partial sums are added with fp64 atomics (like the row-major dense path);
+// returns this thread's share of u'H u.
+template <int RG>
+__device__ __forceinline__ double hess_sym_t(const Op& op, const double* u, double* y) {
+  if (!op.top_owner) return 0.0;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
+  const int n = op.n;
+  double acc = 0.0;
+  for (int ch = gwarp; ch < op.H.nchunks; ch += nwarp) {
+    const int4 cd = __ldg(op.H.chunks + ch);
+    const int rI = cd.x * 64;
+    const double uI0 = (rI + lane < n) ? u[rI + lane] : 0.0;
+    const double uI1 = (rI + 32 + lane < n) ? u[rI + 32 + lane] : 0.0;
+    double ry0 = 0.0, ry1 = 0.0;
+    for (int J = cd.y, t = cd.w; J < cd.z; ++J, ++t) {
+      const double2* tile = reinterpret_cast<const double2*>(op.H.sym + (size_t)t * 4096);
+      const int cJ = J * 64 + 2 * lane;
+      const double uJx = cJ < n ? u[cJ] : 0.0, uJy = cJ + 1 < n ? u[cJ + 1] : 0.0;
+      double cz0 = 0.0, cz1 = 0.0;
+#pragma unroll
+      for (int g = 0; g < 64 / RG; ++g) {
+        double p[RG];
+        double2 a[RG];
+#pragma unroll
+        for (int k = 0; k < RG; ++k) a[k] = __ldg(tile + (g * RG + k) * 32 + lane);
+        const double uIg = (g * RG < 32) ? uI0 : uI1;
+#pragma unroll
+        for (int k = 0; k < RG; ++k) {
+          p[k] = fma(a[k].x, uJx, a[k].y * uJy);
+          const double ur = __shfl_sync(0xffffffffu, uIg, (g * RG + k) & 31);
+          cz0 = fma(a[k].x, ur, cz0);
+          cz1 = fma(a[k].y, ur, cz1);
+        }
+        // transposed butterfly: row g*RG + (lane % RG) ends in p[0]
+        if (RG < 32) {
+#pragma unroll
+          for (int k = 0; k < RG; ++k) p[k] += __shfl_xor_sync(0xffffffffu, p[k], 16);
+        }
+#pragma unroll
+        for (int o = RG / 2; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int k = 0; k < o; ++k) {
+            const double send = up ? p[k] : p[k + o];
+            const double keep = up ? p[k + o] : p[k];
+            p[k] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        // lane l holds row g*RG + (l % RG): keep it in the lane that owns that row
+        const int row = g * RG + (lane % RG);
+        if (row == lane) ry0 += p[0];
+        else if (row == 32 + lane) ry1 += p[0];
+      }
+      if (J != cd.x) {
+        if (cJ < n) { atomicAdd(y + cJ, cz0); acc += uJx * cz0; }
+        if (cJ + 1 < n) { atomicAdd(y + cJ + 1, cz1); acc += uJy * cz1; }
+      }
+    }
+    if (rI + lane < n) { atomicAdd(y + rI + lane, ry0); acc += uI0 * ry0; }
+    if (rI + 32 + lane < n) { atomicAdd(y + rI + 32 + lane, ry1); acc += uI1 * ry1; }
+  }
+  return acc;
+}
+
+#ifndef QPK_SYM_RG
+#define QPK_SYM_RG 32          // tile rows per transposed reduction (32 loads in flight per lane)
+#endif
+__device__ __noinline__ double hess_sym(const Op& op, const double* u, double* y) {
+  return hess_sym_t<QPK_SYM_RG>(op, u, y);
+}
+
 template <int L>
 __device__ __forceinline__ void load_chunk(const Op& op, int k, int e, int4& c, double2& v0, double2& v1) {
   c = make_int4(-1, -1, -1, -1);
@@ -289,7 +381,7 @@ __device__ __forceinline__ double rows_loop_pipelined(const Op& op, double* v, d
   const int nwarp = (gridDim.x * blockDim.x) >> 5;
   const int sub = (threadIdx.x & 31) / L;
   const long long step = (long long)nwarp * RPW;
-  long long rb = (long long)gwarp * RPW;
+  long long rb = op.r0 + (long long)gwarp * RPW;
   int r = (int)rb + sub;
   bool act = rb < op.m && r < op.m;
   int b = 0, e = 0;
@@ -383,7 +475,7 @@ __device__ void phase_rows(const Op& op, double* v, double* y, double* zb,
   const int lane = threadIdx.x & (L - 1);
   constexpr int RPW = 32 / L;                       // rows per warp step
   const int sub_in_warp = (threadIdx.x & 31) / L;
-  for (long long rb = (long long)gwarp * RPW; rb < op.m; rb += (long long)nwarp * RPW) {
+  for (long long rb = op.r0 + (long long)gwarp * RPW; rb < op.m; rb += (long long)nwarp * RPW) {
     const int r = (int)rb + sub_in_warp;
     const bool active = r < op.m;
     int b = 0, e = 0;

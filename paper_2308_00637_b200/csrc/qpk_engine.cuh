@@ -214,8 +214,23 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
   const int N = op.n + op.m, G = E.G;
   double rz = 0.0, acc = 0.0;
   double sacc[QPK_KMAX];
+  double dacc[QPK_DENSE_ROWS_MAX] = {0.0, 0.0, 0.0, 0.0};   // dense B rows: partial c_r . v
+  const int nd = op.ndense;
   const bool lr = op.H.kind == HESS_LOWRANK;
   if (lr) for (int kk = 0; kk < op.H.k; ++kk) sacc[kk] = 0.0;
+  if ((c.mode == MODE_NORMAL || c.mode == MODE_RESTART) && nd && blockIdx.x == 0 && threadIdx.x == 0) {
+    // the fused bottom update of the dense rows (phase_rows skips them)
+    const double* xs = E.x[c.cur];
+    double* xd = E.x[c.xn];
+    for (int r = 0; r < nd; ++r) {
+      const int i = op.n + r;
+      const double dr = __ldg(op.d + r), rr = E.r[i], wr = E.p[i];
+      const double zr = __dmul_rn(1.0 / dr, rr);
+      if (c.xupd) xd[i] = __dadd_rn(xs[i], __dmul_rn(c.alpha_prev, wr));
+      E.p[i] = (c.mode == MODE_RESTART) ? zr : __dadd_rn(zr, __dmul_rn(c.beta, wr));
+      rz += rr * zr;
+    }
+  }
   if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
     // x_t += alpha_prev p_t (lazy), z = M^-1 r, p_t = z (+ beta p_t), y_t = diag(Q) p_t
     const bool restart = c.mode == MODE_RESTART;
@@ -232,6 +247,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
       if (E.panel.cpos) { const int pp = __ldg(E.panel.cpos + j); if (pp >= 0) E.panel.ue[pp] = pn; }
       acc += prep_elem(op, j, pn, E.y);
       if (lr) lowrank_accum(op, j, pn, sacc);
+      for (int q = 0; q < nd; ++q) dacc[q] = fma(__ldg(op.cdense + (size_t)q * op.n + j), pn, dacc[q]);
     }
   } else {
     // CHECK: materialise the pending x_k into x[xn] and prep(x_k).
@@ -248,6 +264,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
         if (E.panel.cpos) { const int pp = __ldg(E.panel.cpos + i); if (pp >= 0) E.panel.ue[pp] = v; }
         acc += prep_elem(op, i, v, E.y);
         if (lr) lowrank_accum(op, i, v, sacc);
+        for (int q = 0; q < nd; ++q) dacc[q] = fma(__ldg(op.cdense + (size_t)q * op.n + i), v, dacc[q]);
       }
     }
   }
@@ -256,6 +273,46 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
   t = block_sum(acc, red);
   if (threadIdx.x == 0) E.part[SLOT_PREP * G + blockIdx.x] = t;
   if (lr) lowrank_flush(op, sacc, E.part, G, red);
+  for (int q = 0; q < nd; ++q) {
+    t = block_sum(dacc[q], red);
+    if (threadIdx.x == 0) E.part[(SLOT_DR + q) * G + blockIdx.x] = t;
+  }
+}
+
+// The dense rows of B after the row pass (same grid as the top kernel):
+// t_r = c_r . v from the top kernel's partials (fixed order, every block gets
+// the same value), z_r = 2 t_r / d_r + w_r, y_b = t_r + d_r w_r (block 0), and
+// y_top += z_r c_r spread over the grid (atomic scatter mode; in CSC mode the
+// column gather reads z_r).  v'Kv gets t z + w y_b.
+template <bool CSC>
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_dense(Engine E, int par) {
+  __shared__ double red[32];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  const Op& op = E.op;
+  const int G = E.G;
+  const double* v = (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
+  double acc = 0.0;
+  for (int q = 0; q < op.ndense; ++q) {
+    const double t = grid_total(E.part + (SLOT_DR + q) * G, G, red);
+    const double dr = __ldg(op.d + q), wr = v[op.n + q];
+    const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, t), dr), wr);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      const double yb = __dadd_rn(t, __dmul_rn(dr, wr));
+      E.y[op.n + q] = yb;
+      E.zb[q] = z;
+      acc += t * z + wr * yb;
+    }
+    if (!CSC) {
+      const double* cr = op.cdense + (size_t)q * op.n;
+      for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < op.n; j += gridDim.x * blockDim.x) {
+        const double a = __ldg(cr + j);
+        if (a != 0.0) atomicAdd(E.y + j, z * a);
+      }
+    }
+  }
+  const double t = block_sum(acc, red);
+  if (threadIdx.x == 0) E.part[SLOT_PREP * G + blockIdx.x] += t;
 }
 
 // ----------------------------------------------------------------- rows ----

@@ -362,11 +362,30 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
       for (int o = LH / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
       if (j < op.n && lh == 0) { E.y[j] += sum; acc += v[j] * sum; }
     }
+  } else if (op.H.kind == HESS_DENSE && op.H.sym) {
+    acc = hess_sym(op, v, E.y);                     // packed symmetric tiles (large dense H)
   } else {
     acc = hess_rows(op, v, E.y, E.part, E.G, red, s_lr);
   }
   const double t = block_sum(acc, red);
   if (threadIdx.x == 0) E.part[SLOT_PREP * E.G + blockIdx.x] += t;
+}
+
+// y_top += H u for a large dense symmetric H from its packed upper tiles
+// (hess_sym_t; its u'Hu partial is added into the slot's PREP partials)
+#ifndef QPK_SYM_MINB
+#define QPK_SYM_MINB 1            // blocks per SM (RG 32: ~250 registers; measured best of RG 16/32 x 1/2)
+#endif
+__global__ void __launch_bounds__(QPK_BLOCK, QPK_SYM_MINB) k_slot_hess_sym(Engine E, int par) {
+  __shared__ double red[32];
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
+  const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
+  const double acc = hess_sym_t<QPK_SYM_RG>(E.op, v, E.y);
+  const double t = block_sum(acc, red);
+  // the grid is sized for the matrix stream, not for the slot's partial layout
+  if (threadIdx.x == 0) atomicAdd(E.part + SLOT_PREP * E.G + blockIdx.x % E.G, t);
 }
 
 // Column sums of the B-tile partials in two deterministic levels, balanced for

@@ -92,3 +92,52 @@ def test_large_hessian_against_oracle():
     h_ref = so.dual_hessian(x, y, 25.0)
     assert np.array_equal(h, h.T)
     assert np.max(np.abs(h - h_ref)) <= 1e-13
+
+
+def test_packed_symmetric_hessian_apply():
+    # n >= QPK_SYM_MIN_N: H is applied from its packed upper tiles (hess_sym);
+    # n = 1100 is not a multiple of the 64-wide tile (zero padding)
+    from oracle import qp_oracle as orc
+    from paper_2308_00637_b200.direction import GpuKkt
+    from paper_2308_00637_b200.problem import build_operator
+    from paper_2308_00637_b200.workloads import _state_from_initial
+    x, y = so.synthetic_dataset(23, 1100, 10)
+    cfg = svm.SvmConfig(sigma=4.0, c=1.0)
+    prob = svm.build_svm_dual(svm.SvmDataset.from_dense(x, y), cfg)
+    host = so.dual_problem(x, y, cfg.sigma, cfg.c)
+    op_h = build_operator(host, _state_from_initial(host))
+    gk = GpuKkt(prob, op_h.bmap)
+    assert gk.ctx.query("hess_sym") == 1
+    gk.set_diagonals(op_h.d_diag, op_h.q_diag_extra)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        v = rng.standard_normal(op_h.dim)
+        y_gpu = gk.apply(v)
+        y_ref = orc.apply_doubly_augmented(op_h, v)
+        assert np.linalg.norm(y_gpu - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
+    # PCG history against the oracle's: 1e-8 until the CPU-reorder envelope
+    # leaves it, then within 10x that envelope (tests/parity.py)
+    import parity
+    rhs = rng.standard_normal(op_h.dim)
+    cfg_p = orc.PcgConfig(tol=1e-300, max_iters=40)
+    xg, info, hist = gk.pcg(rhs, 1e-300, 40, True, history=True)
+    ref_hist = []
+    orc.pcg_direction(op_h, rhs, cfg_p, callback=lambda k, xk, rn: ref_hist.append(rn))
+    h_ref = np.array([np.linalg.norm(rhs)] + ref_hist)
+    assert info.iterations == 40
+    env = parity.envelope(op_h, rhs, cfg_p, h_ref)
+    ok, msg = parity.check_history(hist, h_ref, env)
+    assert ok, msg
+    gk.close()
+
+
+def test_train_packed_matches_oracle_ipm():
+    from oracle import qp_oracle as orc
+    x, y = so.synthetic_dataset(24, 700, 8, sep=3.0)
+    cfg = svm.SvmConfig(sigma=8.0, c=1.0)
+    rep, model = svm.train(svm.SvmDataset.from_dense(x, y), cfg)
+    ref = orc.solve(so.dual_problem(x, y, cfg.sigma, cfg.c), orc.IpmConfig())
+    assert rep.status.value == ref.status
+    assert np.linalg.norm(rep.x - ref.x) <= 1e-6 * max(np.linalg.norm(ref.x), 1.0)
+    assert abs(rep.objective - ref.objective) <= 1e-6 * max(abs(ref.objective), 1.0)
+    assert abs(model.bias - so.bias(x, y, cfg.sigma, cfg.c, ref.x)) <= 1e-5
