@@ -85,7 +85,7 @@ WORKLOAD_DESC = {
     "cfg2": "cfg2 SVM primal d=500, N=50,000 (A = [diag(y)X, y, I], 502 nnz/row)",
     "cfg3": "cfg3 RT-like 200,000 voxels x 20,000 beamlets, 0.5% band density, SparseHessian D_t'D_t",
     "cfg4": "cfg4 RT-like 2,000,000 voxels x 100,000 beamlets, 0.1% band density, SparseHessian D_t'D_t",
-    "svm_dual": "kernel-SVM dual (svm.py:179-195) at the dense-kernel cap: n=20,000 samples, d=100, RBF sigma=100, "
+    "svm_dual": "kernel-SVM dual (svm.py:179-195) at the dense-kernel cap: n=20,000 samples, d=100, RBF sigma=10, "
                 "C=1; H = (y y') * K built on the device (3.2 GB dense), one equality row",
     "cfg5": "cfg5 operator sweep 4,000,000 x 1,000,000, 16 nnz/row, H=diag(U(1e-2,1)), log10 w ~ U(-6,6)",
 }
@@ -101,9 +101,9 @@ def make_workload(name: str, scale: float, seed_offset: int = 0):
         from paper_2308_00637_b200.workloads import _state_from_initial
         x, y = workloads.svm_dual_data(seed=6 + seed_offset, n=int(20_000 * scale), d=100)
         data = svm.SvmDataset.from_dense(x, y)
-        problem = svm.build_svm_dual(data, svm.SvmConfig(sigma=100.0, c=1.0))
+        problem = svm.build_svm_dual(data, svm.SvmConfig(sigma=10.0, c=1.0))
         state = _state_from_initial(problem)
-        meta = {"seed": 6 + seed_offset, "n": len(y), "d": 100, "x": x, "y": y, "sigma": 100.0, "c": 1.0}
+        meta = {"seed": 6 + seed_offset, "n": len(y), "d": 100, "x": x, "y": y, "sigma": 10.0, "c": 1.0}
         rhs = np.random.default_rng(77 + seed_offset).standard_normal(problem.n + 1)
     elif name == "cfg5":
         m, n = int(4_000_000 * scale), int(1_000_000 * scale)
@@ -240,7 +240,7 @@ def run_reference(args):
         from paper_2308_00637_b200.workloads import _state_from_initial, svm_dual_data
         from oracle import svm_oracle as so
         x, y = svm_dual_data(seed=6, n=int(20_000 * args.scale), d=100)
-        problem = so.dual_problem(x, y, 100.0, 1.0)
+        problem = so.dual_problem(x, y, 10.0, 1.0)
         op = build_operator(problem, _state_from_initial(problem))
         rhs = np.random.default_rng(77).standard_normal(op.dim)
         meta = {"seed": 6}

@@ -24,7 +24,8 @@ import sys
 from collections import defaultdict
 from pathlib import Path
 
-SLOT_KERNELS = ("k_slot_top", "k_slot_rows", "k_slot_csc", "k_slot_update", "k_slot_hess", "k_comb_seg",
+SLOT_KERNELS = ("k_slot_top", "k_slot_rows", "k_slot_csc", "k_slot_update", "k_slot_hess", "k_slot_hess_sym",
+                "k_slot_dense", "k_comb_direct", "k_comb_seg",
                 "k_comb_col", "k_slot_panel", "k_panel_comb")
 
 

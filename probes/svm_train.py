@@ -13,7 +13,7 @@ from paper_2308_00637_b200.workloads import svm_dual_data
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
 d = int(sys.argv[2]) if len(sys.argv) > 2 else 100
-sigma = float(sys.argv[3]) if len(sys.argv) > 3 else 100.0
+sigma = float(sys.argv[3]) if len(sys.argv) > 3 else 10.0
 C = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 x, y = svm_dual_data(seed=6, n=n, d=d)
 data = svm.SvmDataset.from_dense(x, y)

@@ -141,3 +141,37 @@ def test_train_packed_matches_oracle_ipm():
     assert np.linalg.norm(rep.x - ref.x) <= 1e-6 * max(np.linalg.norm(ref.x), 1.0)
     assert abs(rep.objective - ref.objective) <= 1e-6 * max(abs(ref.objective), 1.0)
     assert abs(model.bias - so.bias(x, y, cfg.sigma, cfg.c, ref.x)) <= 1e-5
+
+
+@pytest.mark.parametrize("scatter", [1, 2])
+def test_dense_row_split_both_scatter_modes(scatter):
+    # the equality row y'alpha = 0 has n >= 2048 entries: the slot engine
+    # applies it as a dense vector (top-kernel partials + k_slot_dense), in the
+    # atomic (1) and CSC (2) modes; apply, Jacobi and a PCG history vs the oracle
+    import parity
+    from oracle import qp_oracle as orc
+    from paper_2308_00637_b200.direction import GpuKkt
+    from paper_2308_00637_b200.problem import build_operator
+    from paper_2308_00637_b200.workloads import _state_from_initial
+    x, y = so.synthetic_dataset(25, 3000, 6)
+    cfg = svm.SvmConfig(sigma=3.0, c=1.0)
+    prob = svm.build_svm_dual(svm.SvmDataset.from_dense(x, y), cfg)
+    host = so.dual_problem(x, y, cfg.sigma, cfg.c)
+    op_h = build_operator(host, _state_from_initial(host))
+    gk = GpuKkt(prob, op_h.bmap, scatter=scatter)
+    assert gk.ctx.query("dense_rows") == 1 and gk.ctx.query("scatter") == scatter
+    gk.set_diagonals(op_h.d_diag, op_h.q_diag_extra)
+    assert parity.rel_err(gk.jacobi(), orc.jacobi_diagonal(op_h)) <= parity.APPLY_TOL
+    rng = np.random.default_rng(6)
+    v = rng.standard_normal(op_h.dim)
+    assert parity.rel_err(gk.apply(v), orc.apply_doubly_augmented(op_h, v)) <= parity.APPLY_TOL
+    rhs = rng.standard_normal(op_h.dim)
+    cfg_p = orc.PcgConfig(tol=1e-10, max_iters=300)
+    xg, info, hist = gk.pcg(rhs, cfg_p.tol, cfg_p.max_iters, True, history=True)
+    ref_hist = []
+    ref = orc.pcg_direction(op_h, rhs, cfg_p, callback=lambda k, xk, rn: ref_hist.append(rn))
+    h_ref = np.array([np.linalg.norm(rhs)] + ref_hist)
+    ok, msg = parity.check_history(hist, h_ref, parity.envelope(op_h, rhs, cfg_p, h_ref))
+    assert ok, msg
+    assert parity.rel_err(xg, ref.solution) <= 1e-6
+    gk.close()
