@@ -344,7 +344,18 @@ def run_ours(args):
     total_iters = args.iters * args.steps
     value = total_iters / elapsed
 
-    # e2e through the reference-facing drop-in, host buffers
+    # e2e through the reference-facing drop-in, host buffers: the step's inputs
+    # (diagonals, rhs) live in pinned host memory, as a caller staging them
+    # for the GPU would keep them
+    import dataclasses
+
+    def pinned(a):
+        t = torch.empty(len(a), dtype=torch.float64, pin_memory=True)
+        out = t.numpy()
+        out[:] = a
+        return out
+    op = dataclasses.replace(op, d_diag=pinned(op.d_diag), q_diag_extra=pinned(op.q_diag_extra))
+    rhs = pinned(rhs)
     e2e_cfg = PcgConfig(tol=1e-300, max_iters=args.iters)
     if sharded_run:
         from paper_2308_00637_b200.sharded import sharded_direction
