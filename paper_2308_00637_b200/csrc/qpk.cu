@@ -1772,8 +1772,36 @@ static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const
   k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
 }
 
+// Kernel launch with programmatic dependent launch (PDL) allowed: the kernel
+// may be scheduled while its stream predecessor drains (qpk_device.cuh,
+// pdl_wait / pdl_trigger); plain launch when pdl is false
+template <typename... KArgs, typename... Args>
+static void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid; lc.blockDim = block; lc.dynamicSmemBytes = smem; lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at; lc.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&lc, k, args...);
+}
+
+// PDL on the tile-mode slot chain (top -> tile pass -> combine -> update)
+static bool slot_pdl(const qpk_ctx* c) {
+  static const int env = getenv("QPK_PDL") ? atoi(getenv("QPK_PDL")) : 1;
+  return env != 0 && c->scatter == QPK_SCATTER_DICT && !c->sharded;
+}
+
 // CTA-accumulation mode with few partials per column: one combine launch
 static bool comb_direct(const qpk_ctx* c) { return c->scatter == QPK_SCATTER_DICT && c->cacc && c->comb_max2 <= 16; }
+
+// tile mode, single-level combine: the CTA partials are summed inside the
+// update kernel (top_value<3>, same order as k_comb_direct), one launch less
+static bool comb_fused(const qpk_ctx* c) {
+  static const int env = getenv("QPK_FUSE_COMB") ? atoi(getenv("QPK_FUSE_COMB")) : 1;
+  return env != 0 && comb_direct(c) && !c->sharded;
+}
 
 // does the slot finish B'z with a CSC gather pass (k_slot_csc + seg sums)?
 static bool slot_csc(const qpk_ctx* c) {
@@ -1782,7 +1810,8 @@ static bool slot_csc(const qpk_ctx* c) {
 
 static int slot_launches(const qpk_ctx* c) {
   int k = 2;                                                    // top, update
-  if (c->scatter == QPK_SCATTER_DICT) k += (comb_direct(c) ? 2 : 3) + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
+  if (c->scatter == QPK_SCATTER_DICT)
+    k += (comb_fused(c) ? 1 : comb_direct(c) ? 2 : 3) + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
   else if (c->scatter == QPK_SCATTER_PANEL) k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0);
   else k += 1 + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 1 : 0) + (c->n_dense ? 1 : 0);
   if (c->sharded) k += 2;
@@ -1794,7 +1823,8 @@ static int slot_launches(const qpk_ctx* c) {
 static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   const bool csc = slot_csc(c);
   const int G = c->grid_eng;
-  k_slot_top<<<G, QPK_BLOCK, 0, s>>>(E, par);
+  const bool pdl = slot_pdl(c);
+  launch_k(pdl, k_slot_top, dim3(G), dim3(QPK_BLOCK), 0, s, E, par);
   if (c->scatter == QPK_SCATTER_PANEL) {
     QPK_PANEL_DISPATCH(launch_panel_t, c, s, E, par);
     // y_P += B'z (CTA partials); direct remainder: y[col] += yrem
@@ -1804,14 +1834,16 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
     if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   } else if (c->scatter == QPK_SCATTER_DICT) {
-    k_slot_rows_tile<<<E.G_rows, (QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32,
-                       tile_smem(), s>>>(E, par);
-    if (comb_direct(c)) {                                      // y_top += B'z (CTA partials)
-      k_comb_direct<<<std::max(1, std::min(G, (int)((c->n + QPK_BLOCK - 1) / QPK_BLOCK))), QPK_BLOCK, 0, s>>>(
-          E, c->y.p, 1, par);
+    launch_k(pdl, k_slot_rows_tile, dim3(E.G_rows),
+             dim3((QPK_TILE_GROUPS * QPK_TILE_GWARPS + 1 + QPK_TILE_GATHER_WARPS) * 32), tile_smem(), s, E, par);
+    if (comb_fused(c)) {
+      // y_top's B'z partials are summed by the update kernel (k_slot_update<3>)
+    } else if (comb_direct(c)) {                               // y_top += B'z (CTA partials)
+      launch_k(pdl, k_comb_direct, dim3(std::max(1, std::min(G, (int)((c->n + QPK_BLOCK - 1) / QPK_BLOCK)))),
+               dim3(QPK_BLOCK), 0, s, E, c->y.p, 1, par);
     } else {
-      k_comb_seg<<<G, QPK_BLOCK, 0, s>>>(E, par);             // y_top += B'z (tile partials)
-      k_comb_col<<<G, QPK_BLOCK, 0, s>>>(E, c->y.p, 1, par);
+      launch_k(pdl, k_comb_seg, dim3(G), dim3(QPK_BLOCK), 0, s, E, par);     // y_top += B'z (tile partials)
+      launch_k(pdl, k_comb_col, dim3(G), dim3(QPK_BLOCK), 0, s, E, c->y.p, 1, par);
     }
     if (c->hkind != QPK_HESS_DIAG && !c->h_tiled) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
   } else {
@@ -1845,7 +1877,8 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   launch_slot_apply(c, E, par, s);
   if (!c->sharded) {
     if (csc) k_slot_update<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
-    else k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+    else if (comb_fused(c)) launch_k(slot_pdl(c), k_slot_update<3>, dim3(G), dim3(QPK_BLOCK), 0, s, E, par);
+    else launch_k(slot_pdl(c), k_slot_update<1>, dim3(G), dim3(QPK_BLOCK), 0, s, E, par);
     return;
   }
   // sharded: finish the local top block and scalars, one grouped all-reduce
@@ -1877,6 +1910,7 @@ static int apply_engine(qpk_ctx* c, const double* v_dev, double* y_dev) {
   Engine E = make_engine(c);
   launch_slot_apply(c, E, 0, s);
   if (slot_csc(c)) k_apply_finish<2><<<c->grid_eng, QPK_BLOCK, 0, s>>>(E, y_dev);
+  else if (comb_fused(c)) k_apply_finish<3><<<c->grid_eng, QPK_BLOCK, 0, s>>>(E, y_dev);
   else k_apply_finish<1><<<c->grid_eng, QPK_BLOCK, 0, s>>>(E, y_dev);
   c->launches += slot_launches(c) - 1;
   CUDA_TRY(cudaGetLastError());

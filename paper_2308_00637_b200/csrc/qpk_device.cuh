@@ -76,6 +76,16 @@ __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   return r;
 }
 
+// ------------------------------------------------ programmatic launch ----
+// Programmatic dependent launch (PDL): a kernel launched with the
+// programmatic-serialisation attribute may be scheduled while its predecessor
+// drains; it must not touch the predecessor's outputs before pdl_wait().  A
+// kernel triggers its dependent only after its own pdl_wait(), so code before
+// pdl_wait() may read anything produced two or more kernels back.  Both are
+// no-ops for kernels launched without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ----------------------------------------------------------- reductions ----
 // Sum over the calling block; result broadcast to every thread.  Fixed tree:
 // deterministic for a fixed blockDim.

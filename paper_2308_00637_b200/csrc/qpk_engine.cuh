@@ -207,6 +207,8 @@ __global__ void k_engine_init2(Engine E) {
 // ------------------------------------------------------------------ top ----
 __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
   __shared__ double red[32];
+  pdl_wait();
+  pdl_trigger();
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_top = globaltimer_ns();
@@ -487,6 +489,8 @@ template <int SC>
 __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
   constexpr bool CSC = SC != 1;
   __shared__ double red[32];
+  pdl_wait();
+  pdl_trigger();
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) {
     if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par ^ 1] = c;

@@ -149,6 +149,11 @@ k_slot_rows_tile(Engine E, int par) {
   double pacc = 0.0, rzb = 0.0;
   if (warp == CW) {
     // ---------------------------------------------------------- producer ----
+    // In a PCG iteration (fuse) it streams only data written two or more
+    // kernels back (the matrix, d, and the bottom windows of p, r, x[cur]), so
+    // under programmatic launch the ring fills while the top kernel is still
+    // running; in CHECK / FINAL the top kernel materialises the x it reads.
+    if (!fuse) pdl_wait();
     if (lane == 0) {
       const double* wsrc = v;
       const double* xsrc = E.x[c.cur];
@@ -185,6 +190,8 @@ k_slot_rows_tile(Engine E, int par) {
     }
   } else if (warp > CW) {
     // ----------------------------------------------------- gather warps ----
+    pdl_wait();                                        // u = p_top comes from the top kernel
+    pdl_trigger();
     // u[cols] for each landed tile (warp CW+1+k takes tiles it = k mod NGW),
     // 8 independent gathers in flight per lane, then "u ready"
     constexpr int NGW = QPK_TILE_GATHER_WARPS;
@@ -224,6 +231,8 @@ k_slot_rows_tile(Engine E, int par) {
     }
   } else {
     // ---------------------------------------------------------- consumers ---
+    pdl_wait();                                        // y_top is initialised by the top kernel
+    pdl_trigger();
     constexpr int T = QPK_TILE_GWARPS * 32;          // threads per group
     const int g = warp / QPK_TILE_GWARPS, gw = warp % QPK_TILE_GWARPS;
     const int tid = threadIdx.x - g * T;
@@ -395,6 +404,8 @@ __global__ void __launch_bounds__(QPK_BLOCK, QPK_SYM_MINB) k_slot_hess_sym(Engin
 //   k_comb_col:  out[j] (+)= sum of column j's segment sums, in order
 #define QPK_COMB_CHUNK 128
 __global__ void __launch_bounds__(QPK_BLOCK) k_comb_seg(Engine E, int par) {
+  pdl_wait();
+  pdl_trigger();
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
   if (par >= 0 && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_mid = globaltimer_ns();
   const int LC = E.dict.comb_lanes, lc = threadIdx.x & (LC - 1);
@@ -420,6 +431,8 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_comb_seg(Engine E, int par) {
 }
 
 __global__ void __launch_bounds__(QPK_BLOCK) k_comb_col(Engine E, double* out, int add, int par) {
+  pdl_wait();
+  pdl_trigger();
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x) {
     const int qb = __ldg(E.dict.col_seg + j), qe = __ldg(E.dict.col_seg + j + 1);
@@ -433,6 +446,8 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_comb_col(Engine E, double* out, i
 // a few CTA partials (banded B: the CTAs whose tile range meets the column's
 // band): out[j] (+)= sum of column j's partials in CTA order, thread per column.
 __global__ void __launch_bounds__(QPK_BLOCK) k_comb_direct(Engine E, double* out, int add, int par) {
+  pdl_wait();
+  pdl_trigger();
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
   if (par >= 0 && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_mid = globaltimer_ns();
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x) {
