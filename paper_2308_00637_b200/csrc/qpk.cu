@@ -662,12 +662,28 @@ static void launch_jac_rows(int lanes, int grid, cudaStream_t s, const Op& o, do
   }
 }
 
+// Kernel launch with programmatic dependent launch (PDL) allowed: the kernel
+// may be scheduled while its stream predecessor drains (qpk_device.cuh,
+// pdl_wait / pdl_trigger); plain launch when pdl is false
+template <typename... KArgs, typename... Args>
+static void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     Args... args) {
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid; lc.blockDim = block; lc.dynamicSmemBytes = smem; lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at; lc.numAttrs = pdl ? 1 : 0;
+  cudaLaunchKernelEx(&lc, k, args...);
+}
+
 static const int kPanelQ[] = {1, 2, 4, 6, 8, 12, 16};
 
 
 template <int Q>
-static void launch_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E, int par) {
-  k_slot_panel<Q><<<c->panel_grid, QPK_PANEL_CW * 32, panel_smem_bytes(c->panel_kp, c->panel_ew), s>>>(E, par);
+static void launch_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E, int par, bool pdl) {
+  launch_k(pdl, k_slot_panel<Q>, dim3(c->panel_grid), dim3(QPK_PANEL_CW * 32),
+           panel_smem_bytes(c->panel_kp, c->panel_ew), s, E, par);
 }
 template <int Q>
 static void launch_jac_panel_t(const qpk_ctx* c, cudaStream_t s, const Engine& E) {
@@ -1772,25 +1788,11 @@ static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const
   k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
 }
 
-// Kernel launch with programmatic dependent launch (PDL) allowed: the kernel
-// may be scheduled while its stream predecessor drains (qpk_device.cuh,
-// pdl_wait / pdl_trigger); plain launch when pdl is false
-template <typename... KArgs, typename... Args>
-static void launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                     Args... args) {
-  cudaLaunchConfig_t lc = {};
-  lc.gridDim = grid; lc.blockDim = block; lc.dynamicSmemBytes = smem; lc.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  lc.attrs = at; lc.numAttrs = pdl ? 1 : 0;
-  cudaLaunchKernelEx(&lc, k, args...);
-}
-
-// PDL on the tile-mode slot chain (top -> tile pass -> combine -> update)
+// PDL on the tile / panel slot chains (top -> pass over B -> combine -> update)
 static bool slot_pdl(const qpk_ctx* c) {
   static const int env = getenv("QPK_PDL") ? atoi(getenv("QPK_PDL")) : 1;
-  return env != 0 && c->scatter == QPK_SCATTER_DICT && !c->sharded;
+  return env != 0 && !c->sharded &&
+         (c->scatter == QPK_SCATTER_DICT || (c->scatter == QPK_SCATTER_PANEL && c->panel_direct));
 }
 
 // CTA-accumulation mode with few partials per column: one combine launch
@@ -1826,11 +1828,11 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
   const bool pdl = slot_pdl(c);
   launch_k(pdl, k_slot_top, dim3(G), dim3(QPK_BLOCK), 0, s, E, par);
   if (c->scatter == QPK_SCATTER_PANEL) {
-    QPK_PANEL_DISPATCH(launch_panel_t, c, s, E, par);
+    QPK_PANEL_DISPATCH(launch_panel_t, c, s, E, par, pdl);
     // y_P += B'z (CTA partials); direct remainder: y[col] += yrem
     const int rem_blocks = (c->panel_direct && c->panel_ew > 0)
                                ? (int)std::min<long long>(2 * c->sms, (c->m * c->panel_ew + 1023) / 1024) : 0;
-    k_panel_comb<<<c->panel_kp / 32 + rem_blocks, 1024, 0, s>>>(E, c->y.p, 1, par);
+    launch_k(pdl, k_panel_comb, dim3(c->panel_kp / 32 + rem_blocks), dim3(1024), 0, s, E, c->y.p, 1, par);
     if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   } else if (c->scatter == QPK_SCATTER_DICT) {

@@ -104,6 +104,8 @@ template <int Q>
 __global__ void __launch_bounds__(QPK_PANEL_CW * 32, 1) k_slot_panel(Engine E, int par) {
   extern __shared__ __align__(128) double psm[];
   constexpr int S = QPK_PANEL_STAGES, CW = QPK_PANEL_CW, RPW = PanelRpw<Q>::value;
+  pdl_wait();                                    // the top kernel stages u (p_top, remainder u values)
+  pdl_trigger();
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_rows = globaltimer_ns();
@@ -314,6 +316,8 @@ __global__ void __launch_bounds__(QPK_PANEL_CW * 32, 1) k_slot_panel(Engine E, i
 // the 8 warp sums are then added in warp order.
 __global__ void __launch_bounds__(1024) k_panel_comb(Engine E, double* out, int add, int par) {
   __shared__ double ws[32][33];
+  pdl_wait();
+  pdl_trigger();
   if (par >= 0 && E.ctrl[par].mode == MODE_DONE) return;
   if (par >= 0 && blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_mid = globaltimer_ns();
   const Panel& P = E.panel;
