@@ -485,6 +485,9 @@ __device__ __forceinline__ void decide(const Engine& E, const Ctrl& c, int par, 
 }
 
 // --------------------------------------------------------------- update ----
+#ifndef QPK_UPD_U
+#define QPK_UPD_U 4               // independent double2 pairs in flight per thread
+#endif
 template <int SC>
 __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
   constexpr bool CSC = SC != 1;
@@ -531,39 +534,56 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       return;
     }
     alpha = rz / pap;
-    if (!CSC) {
-      const int np = N >> 1;
+    // scalar head: top entries whose y needs its column partials (CSC / tile
+    // modes), rounded up to an even index so the rest runs on double2 pairs
+    const int nb = CSC ? min(N, (op.n + 1) & ~1) : 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+      const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
+      const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
+      E.r[i] = ri;
+      if (op.top_owner || i >= op.n) {
+        rr += ri * ri;
+        rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
+      }
+    }
+    // pairs: QPK_UPD_U independent pairs per thread with every load issued
+    // before the first store (r is read and written, so the compiler cannot
+    // hoist the next iteration's loads on its own)
+    {
+      constexpr int U = QPK_UPD_U;
+      const int p0 = nb >> 1, np = N >> 1;
+      const int stride = gridDim.x * blockDim.x;
       double2* r2 = reinterpret_cast<double2*>(E.r);
       const double2* y2 = reinterpret_cast<const double2*>(E.y);
       const double2* m2 = reinterpret_cast<const double2*>(E.minv);
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
-        double2 ri = r2[i];
-        const double2 yi = y2[i];
-        const double2 mi = __ldg(m2 + i);
-        ri.x = __dsub_rn(ri.x, __dmul_rn(alpha, yi.x));
-        ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yi.y));
-        r2[i] = ri;
-        // replicated top entries count once over the ranks (rank 0)
-        const bool cx = op.top_owner || 2 * i >= op.n, cy = op.top_owner || 2 * i + 1 >= op.n;
-        if (cx) { rr += ri.x * ri.x; rzn += ri.x * __dmul_rn(mi.x, ri.x); }
-        if (cy) { rr += ri.y * ri.y; rzn += ri.y * __dmul_rn(mi.y, ri.y); }
+      for (int base = p0 + blockIdx.x * blockDim.x + threadIdx.x; base < np; base += U * stride) {
+        double2 rv[U], yv[U], mv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * stride;
+          if (i < np) { rv[u] = r2[i]; yv[u] = __ldg(y2 + i); mv[u] = __ldg(m2 + i); }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int i = base + u * stride;
+          if (i < np) {
+            double2 ri = rv[u];
+            ri.x = __dsub_rn(ri.x, __dmul_rn(alpha, yv[u].x));
+            ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yv[u].y));
+            r2[i] = ri;
+            // replicated top entries count once over the ranks (rank 0)
+            const bool cx = op.top_owner || 2 * i >= op.n, cy = op.top_owner || 2 * i + 1 >= op.n;
+            if (cx) { rr += ri.x * ri.x; rzn += ri.x * __dmul_rn(mv[u].x, ri.x); }
+            if (cy) { rr += ri.y * ri.y; rzn += ri.y * __dmul_rn(mv[u].y, ri.y); }
+          }
+        }
       }
-      if ((N & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+      if ((N & 1) && N - 1 >= nb && blockIdx.x == 0 && threadIdx.x == 0) {
         const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
         E.r[N - 1] = ri;
         if (op.top_owner || N - 1 >= op.n) {
           rr += ri * ri;
           rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
-        }
-      }
-    } else {
-      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-        const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
-        const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
-        E.r[i] = ri;
-        if (op.top_owner || i >= op.n) {
-          rr += ri * ri;
-          rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
         }
       }
     }
