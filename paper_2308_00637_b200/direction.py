@@ -153,8 +153,12 @@ def operator_for(op, device: int = 0) -> GpuKkt:
     problem = op.problem
     key = id(problem)
     entry = _CACHE.get(key)
-    if entry is not None and entry[0]() is problem and entry[2] == _bmap_key(op.bmap):
-        return entry[1]
+    if entry is not None and entry[0]() is problem:
+        # the reference hands the same bound-index arrays to every IPM
+        # iteration: identical objects skip hashing them (1.6M indices on cfg4)
+        same = entry[3][0] is op.bmap.lin_lower and entry[3][1] is op.bmap.lin_upper
+        if same or entry[2] == _bmap_key(op.bmap):
+            return entry[1]
     if entry is not None:
         _finalizer(key)
     gk = GpuKkt(problem, op.bmap, device=device)
@@ -162,7 +166,7 @@ def operator_for(op, device: int = 0) -> GpuKkt:
         ref = weakref.ref(problem, lambda _r, k=key: _finalizer(k))
     except TypeError:
         ref = lambda p=problem: p  # noqa: E731  (unweakrefable problem: keep it alive)
-    _CACHE[key] = (ref, gk, _bmap_key(op.bmap))
+    _CACHE[key] = (ref, gk, _bmap_key(op.bmap), (op.bmap.lin_lower, op.bmap.lin_upper))
     return gk
 
 
