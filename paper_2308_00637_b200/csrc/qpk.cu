@@ -1092,6 +1092,7 @@ static int build_dict(qpk_ctx* c) {
                                    hperm.data());
     if (hs > 0 && (double)c->h_hci.size() / (double)hs >= 0.5) {
       c->h_tiled = true;
+      hperm.resize(hperm.size() + 4, 0);               // the tile kernel bulk-copies 16-byte windows
       CUDA_TRY(upload(c->hperm, hperm, c->stream));
     } else {
       tiles.resize(t0); cols.resize(c0); tval.resize(v0); tid = n_btiles;

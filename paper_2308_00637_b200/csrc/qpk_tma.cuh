@@ -88,7 +88,13 @@ struct alignas(16) DTileStage {
 #ifndef QPK_TILE_GWARPS
 #define QPK_TILE_GWARPS 4        // warps per consumer group
 #endif
-#define QPK_TILE_GATHER_WARPS 2  // warps gathering u[cols] for landed tiles
+#ifndef QPK_TILE_GATHER_WARPS
+#define QPK_TILE_GATHER_WARPS 3  // warps gathering u[cols] for landed tiles (must divide QPK_TILE_STAGES)
+#endif
+// a ring stage is always reused by the warp / group that used it last, so an
+// mbarrier parity wait can never be satisfied by a phase two uses old
+static_assert(QPK_TILE_STAGES % QPK_TILE_GATHER_WARPS == 0, "gather warps must divide the ring stages");
+static_assert(QPK_TILE_STAGES % QPK_TILE_GROUPS == 0, "consumer groups must divide the ring stages");
 #ifndef QPK_TILE_UMAX
 #define QPK_TILE_UMAX 1024       // CTA-accumulator capacity (distinct columns of a CTA's tiles)
 #endif
@@ -97,7 +103,7 @@ struct DTileSmem {
   DTileStage st[QPK_TILE_STAGES];
   unsigned long long full[QPK_TILE_STAGES], empty[QPK_TILE_STAGES], uready[QPK_TILE_STAGES];
   double rpart[QPK_TILE_GROUPS][QPK_TILE_GWARPS][QPK_TILE_ROWS];
-  double zs[QPK_TILE_GROUPS][QPK_TILE_ROWS];
+  alignas(16) double zs[QPK_TILE_GROUPS][QPK_TILE_ROWS];
   double red[32];
   double s_lr[QPK_KMAX];
 };
@@ -154,15 +160,38 @@ k_slot_rows_tile(Engine E, int par) {
     // under programmatic launch the ring fills while the top kernel is still
     // running; in CHECK / FINAL the top kernel materialises the x it reads.
     if (!fuse) pdl_wait();
-    if (lane == 0) {
-      const double* wsrc = v;
-      const double* xsrc = E.x[c.cur];
-      for (int it = 0; it < my; ++it) {
-        const int t = tb + it * tstep;
+    // Tile descriptors are prefetched a warp-batch ahead: lane l holds the
+    // descriptor of tile (batch + l) and lane 0 takes them by shuffle, so no
+    // dependent descriptor load sits between a stage's release and its refill.
+    const double* wsrc = v;
+    const double* xsrc = E.x[c.cur];
+    auto ld_desc = [&](int base) {
+      int4 lo = make_int4(0, 0, 0, 0), hi = lo;
+      const int k = base + lane;
+      if (k < my) {
+        const int4* q = reinterpret_cast<const int4*>(D.tiles + tb + (long long)k * tstep);
+        lo = __ldg(q);
+        hi = __ldg(q + 1);
+      }
+      return TileDescD{lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    };
+    TileDescD cur_b = ld_desc(0), nxt_b = ld_desc(32);
+    for (int it = 0; it < my; ++it) {
+      const int l = it & 31;
+      if (l == 0 && it > 0) { cur_b = nxt_b; nxt_b = ld_desc(it + 32); }
+      TileDescD td;
+      td.ra = __shfl_sync(0xffffffffu, cur_b.ra, l);
+      td.rb = __shfl_sync(0xffffffffu, cur_b.rb, l);
+      td.d0 = __shfl_sync(0xffffffffu, cur_b.d0, l);
+      td.ndp = __shfl_sync(0xffffffffu, cur_b.ndp, l);
+      td.v0 = __shfl_sync(0xffffffffu, cur_b.v0, l);
+      td.pad0 = __shfl_sync(0xffffffffu, cur_b.pad0, l);
+      td.pad1 = __shfl_sync(0xffffffffu, cur_b.pad1, l);
+      td.pad2 = __shfl_sync(0xffffffffu, cur_b.pad2, l);
+      if (lane == 0) {
         const int s = it % QPK_TILE_STAGES;
         mbar_wait(&S.empty[s], ((it / QPK_TILE_STAGES) & 1) ^ 1);
         DTileStage& st = S.st[s];
-        const TileDescD td = D.tiles[t];
         st.t = td;
         const int v0 = td.ra & ~1, w0 = (op.n + td.ra) & ~1;
         st.v0 = v0;
@@ -170,23 +199,35 @@ k_slot_rows_tile(Engine E, int par) {
         const uint32_t b_a = round_up16((uint32_t)((td.rb - td.ra) * td.pad0) * 8u);
         const uint32_t b_c = round_up16((uint32_t)td.ndp * 4u);
         if (td.pad1) {                                  // Hessian tile: no per-row vectors
-          mbar_expect_tx(&S.full[s], b_a + b_c);
+          // (its row ids hperm[ra .. rb) land in st.d, from a 16-byte aligned start)
+          const uint32_t b_j = D.hperm ? round_up16((uint32_t)(td.rb - (td.ra & ~3)) * 4u) : 0u;
+          mbar_expect_tx(&S.full[s], b_a + b_c + b_j);
           bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
           bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
-          continue;
-        }
-        const uint32_t b_d = round_up16((uint32_t)(((td.rb + 1) & ~1) - v0) * 8u);
-        const uint32_t b_w = round_up16((uint32_t)(((op.n + td.rb + 1) & ~1) - w0) * 8u);
-        mbar_expect_tx(&S.full[s], b_a + b_c + b_d + b_w + (fuse ? 2 * b_w : 0u));
-        bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
-        bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
-        bulk_g2s(st.d, op.d + v0, b_d, &S.full[s]);
-        bulk_g2s(st.w, wsrc + w0, b_w, &S.full[s]);
-        if (fuse) {
-          bulk_g2s(st.r, E.r + w0, b_w, &S.full[s]);
-          bulk_g2s(st.x, xsrc + w0, b_w, &S.full[s]);
+          if (b_j) bulk_g2s(st.d, D.hperm + (td.ra & ~3), b_j, &S.full[s]);
+        } else {
+          const uint32_t b_d = round_up16((uint32_t)(((td.rb + 1) & ~1) - v0) * 8u);
+          const uint32_t b_w = round_up16((uint32_t)(((op.n + td.rb + 1) & ~1) - w0) * 8u);
+#ifdef QPK_TSLOT_TMA
+          // CTA accumulation: the tile's accumulator slots land in the upper
+          // half of ud (the gather warps read them before overwriting it)
+          const uint32_t b_s = D.cacc ? b_c : 0u;
+#else
+          const uint32_t b_s = 0u;
+#endif
+          mbar_expect_tx(&S.full[s], b_a + b_c + b_s + b_d + b_w + (fuse ? 2 * b_w : 0u));
+          bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
+          bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
+          if (b_s) bulk_g2s(st.ud + QPK_TILE_DMAX / 2, D.tslot + td.d0, b_s, &S.full[s]);
+          bulk_g2s(st.d, op.d + v0, b_d, &S.full[s]);
+          bulk_g2s(st.w, wsrc + w0, b_w, &S.full[s]);
+          if (fuse) {
+            bulk_g2s(st.r, E.r + w0, b_w, &S.full[s]);
+            bulk_g2s(st.x, xsrc + w0, b_w, &S.full[s]);
+          }
         }
       }
+      __syncwarp();
     }
   } else if (warp > CW) {
     // ----------------------------------------------------- gather warps ----
@@ -205,6 +246,25 @@ k_slot_rows_tile(Engine E, int par) {
       // gathered, so its slots in the CTA accumulator replace it in place)
       const bool slots = D.cacc && !st.t.pad1;
       const int d0 = st.t.d0;
+      // Hessian tile: its rows are top indices j (hperm window in st.d); stage
+      // u_j and the current y_j (this tile is y_j's only writer in the pass)
+      // in the row arrays the TMA leaves unused for such tiles, so the
+      // consumers' row finish has no dependent global loads
+      const bool hrows = st.t.pad1;
+      const int hra = st.t.ra, hR = st.t.rb - st.t.ra;
+      const int* jrow = reinterpret_cast<const int*>(st.d) + (hra & 3);
+      double hu[2] = {0.0, 0.0}, hy[2] = {0.0, 0.0};
+      if (hrows) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rr = lane + 32 * q;
+          if (rr < hR) {
+            const int j = D.hperm ? jrow[rr] : hra + rr;
+            hu[q] = u[j];
+            hy[q] = E.y[j];
+          }
+        }
+      }
       for (int cb = lane; cb < nd; cb += 32 * 8) {
         double g8[8];
         int s8[8];
@@ -213,7 +273,11 @@ k_slot_rows_tile(Engine E, int par) {
           const int cc = cb + 32 * q;
           const int col = cc < nd ? st.cols[cc] : -1;
           g8[q] = col >= 0 ? u[col] : 0.0;
+#ifdef QPK_TSLOT_TMA
+          s8[q] = (slots && cc < nd) ? reinterpret_cast<const int*>(st.ud + QPK_TILE_DMAX / 2)[cc] : -1;
+#else
           s8[q] = (slots && cc < nd) ? __ldg(D.tslot + d0 + cc) : -1;
+#endif
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -224,8 +288,19 @@ k_slot_rows_tile(Engine E, int par) {
           }
         }
       }
+      // Hessian tile: its rows are top indices j = hperm[ra + rr]; stage j,
+      // u_j and the current y_j (this tile is y_j's only writer in the pass)
+      // in the row arrays the TMA leaves unused for such tiles, so the
+      // consumers' row finish has no dependent global loads
+      if (hrows) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int rr = lane + 32 * q;
+          if (rr < hR) { st.w[rr] = hu[q]; st.x[rr] = hy[q]; }
+        }
+      }
       // generic-proxy writes into a stage the TMA (async proxy) refills later
-      if (slots) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (slots || hrows) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&S.uready[s]);
     }
@@ -266,9 +341,9 @@ k_slot_rows_tile(Engine E, int par) {
           double tt = 0.0;
 #pragma unroll
           for (int ww = 0; ww < QPK_TILE_GWARPS; ++ww) tt += S.rpart[g][ww][rr];
-          const int j = D.hperm ? __ldg(D.hperm + td.ra + rr) : td.ra + rr;
-          E.y[j] += tt;
-          pacc += v[j] * tt;
+          const int j = D.hperm ? reinterpret_cast<const int*>(st.d)[(td.ra & 3) + rr] : td.ra + rr;
+          E.y[j] = st.x[rr] + tt;                         // y_j and u_j staged by the gather warps
+          pacc += st.w[rr] * tt;
         }
         tile_group_bar(g);                              // rpart is rewritten by the next tile
         __syncwarp();
@@ -298,6 +373,26 @@ k_slot_rows_tile(Engine E, int par) {
         S.zs[g][rr] = z;
       }
       tile_group_bar(g);
+#ifdef QPK_COLPASS4
+      // column pass: 4 rows per step (4 independent chains, z read as
+      // broadcast double2 pairs, the column walked by pointer increments)
+      const double2* z2 = reinterpret_cast<const double2*>(S.zs[g]);
+      for (int cc = tid; cc < nd; cc += T) {
+        const double* ap = st.a + cc;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int rr = 0;
+        for (; rr + 3 < R; rr += 4) {
+          const double2 za = z2[rr >> 1], zb = z2[(rr >> 1) + 1];
+          const double a0 = ap[0], a1 = ap[pitch], a2 = ap[2 * pitch], a3 = ap[3 * pitch];
+          s0 = fma(a0, za.x, s0);
+          s1 = fma(a1, za.y, s1);
+          s2 = fma(a2, zb.x, s2);
+          s3 = fma(a3, zb.y, s3);
+          ap += 4 * pitch;
+        }
+        for (; rr < R; ++rr, ap += pitch) s0 = fma(*ap, S.zs[g][rr], s0);
+        const double colsum = (s0 + s1) + (s2 + s3);
+#else
       for (int cc = tid; cc < nd; cc += T) {
         double s0 = 0.0, s1 = 0.0;
         int rr = 0;
@@ -306,11 +401,13 @@ k_slot_rows_tile(Engine E, int par) {
           s1 = fma(st.a[(rr + 1) * pitch + cc], S.zs[g][rr + 1], s1);
         }
         if (rr < R) s0 = fma(st.a[rr * pitch + cc], S.zs[g][rr], s0);
+        const double colsum = s0 + s1;
+#endif
         if (D.cacc) {
           const int sl = st.cols[cc];                     // slot (gather warps), distinct per tile column
-          if (sl >= 0) cacc[g * QPK_TILE_UMAX + sl] += s0 + s1;
+          if (sl >= 0) cacc[g * QPK_TILE_UMAX + sl] += colsum;
         } else {
-          D.bpart[td.d0 + cc] = s0 + s1;
+          D.bpart[td.d0 + cc] = colsum;
         }
       }
       __syncwarp();

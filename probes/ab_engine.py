@@ -44,7 +44,7 @@ def main():
                 ph = [round(v * 1e3 / iters, 1) for v in info.phase_ms]
                 print(f"{name} {Path(lib).name} scatter={mode} engine={gk.ctx.query('engine')} "
                       f"grid={gk.ctx.query('grid_engine')}: {1e3 / best:.0f} it/s ({best * 1e3:.1f} us/it) "
-                      f"phases {ph}", flush=True)
+                      f"phases {ph} iters {info.iterations}", flush=True)
                 gk.close()
 
 
