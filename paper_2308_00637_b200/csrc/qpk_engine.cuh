@@ -391,9 +391,21 @@ __device__ __forceinline__ double top_value(const Engine& E, int j) {
     const int qb = __ldg(E.seg_ptr + j), qe = __ldg(E.seg_ptr + j + 1);
     for (int q = qb; q < qe; ++q) s += E.seg_sum[q];
   } else if (SC == 3) {
+    // 8 partial positions, then 8 partials in flight per round trip; the sum
+    // keeps the partial order (bitwise the same as one at a time)
     const int qb = __ldg(E.dict.col_ptr + j), qe = __ldg(E.dict.col_ptr + j + 1);
     const double* src = E.dict.cacc ? E.dict.cpart : E.dict.bpart;
-    for (int q = qb; q < qe; ++q) s += src[__ldg(E.dict.col_pos + q)];
+    for (int q = qb; q < qe; q += 8) {
+      int pos[8];
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) pos[k] = (q + k < qe) ? __ldg(E.dict.col_pos + q + k) : -1;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = (pos[k] >= 0) ? src[pos[k]] : 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (q + k < qe) s += v[k];
+    }
   }
   return E.y[j] + s;
 }

@@ -208,17 +208,9 @@ k_slot_rows_tile(Engine E, int par) {
         } else {
           const uint32_t b_d = round_up16((uint32_t)(((td.rb + 1) & ~1) - v0) * 8u);
           const uint32_t b_w = round_up16((uint32_t)(((op.n + td.rb + 1) & ~1) - w0) * 8u);
-#ifdef QPK_TSLOT_TMA
-          // CTA accumulation: the tile's accumulator slots land in the upper
-          // half of ud (the gather warps read them before overwriting it)
-          const uint32_t b_s = D.cacc ? b_c : 0u;
-#else
-          const uint32_t b_s = 0u;
-#endif
-          mbar_expect_tx(&S.full[s], b_a + b_c + b_s + b_d + b_w + (fuse ? 2 * b_w : 0u));
+          mbar_expect_tx(&S.full[s], b_a + b_c + b_d + b_w + (fuse ? 2 * b_w : 0u));
           bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
           bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
-          if (b_s) bulk_g2s(st.ud + QPK_TILE_DMAX / 2, D.tslot + td.d0, b_s, &S.full[s]);
           bulk_g2s(st.d, op.d + v0, b_d, &S.full[s]);
           bulk_g2s(st.w, wsrc + w0, b_w, &S.full[s]);
           if (fuse) {
@@ -273,11 +265,7 @@ k_slot_rows_tile(Engine E, int par) {
           const int cc = cb + 32 * q;
           const int col = cc < nd ? st.cols[cc] : -1;
           g8[q] = col >= 0 ? u[col] : 0.0;
-#ifdef QPK_TSLOT_TMA
-          s8[q] = (slots && cc < nd) ? reinterpret_cast<const int*>(st.ud + QPK_TILE_DMAX / 2)[cc] : -1;
-#else
           s8[q] = (slots && cc < nd) ? __ldg(D.tslot + d0 + cc) : -1;
-#endif
         }
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
@@ -373,26 +361,6 @@ k_slot_rows_tile(Engine E, int par) {
         S.zs[g][rr] = z;
       }
       tile_group_bar(g);
-#ifdef QPK_COLPASS4
-      // column pass: 4 rows per step (4 independent chains, z read as
-      // broadcast double2 pairs, the column walked by pointer increments)
-      const double2* z2 = reinterpret_cast<const double2*>(S.zs[g]);
-      for (int cc = tid; cc < nd; cc += T) {
-        const double* ap = st.a + cc;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int rr = 0;
-        for (; rr + 3 < R; rr += 4) {
-          const double2 za = z2[rr >> 1], zb = z2[(rr >> 1) + 1];
-          const double a0 = ap[0], a1 = ap[pitch], a2 = ap[2 * pitch], a3 = ap[3 * pitch];
-          s0 = fma(a0, za.x, s0);
-          s1 = fma(a1, za.y, s1);
-          s2 = fma(a2, zb.x, s2);
-          s3 = fma(a3, zb.y, s3);
-          ap += 4 * pitch;
-        }
-        for (; rr < R; ++rr, ap += pitch) s0 = fma(*ap, S.zs[g][rr], s0);
-        const double colsum = (s0 + s1) + (s2 + s3);
-#else
       for (int cc = tid; cc < nd; cc += T) {
         double s0 = 0.0, s1 = 0.0;
         int rr = 0;
@@ -402,7 +370,6 @@ k_slot_rows_tile(Engine E, int par) {
         }
         if (rr < R) s0 = fma(st.a[rr * pitch + cc], S.zs[g][rr], s0);
         const double colsum = s0 + s1;
-#endif
         if (D.cacc) {
           const int sl = st.cols[cc];                     // slot (gather warps), distinct per tile column
           if (sl >= 0) cacc[g * QPK_TILE_UMAX + sl] += colsum;
