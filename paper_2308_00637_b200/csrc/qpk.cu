@@ -1952,10 +1952,17 @@ static Engine make_engine(qpk_ctx* c) {
   E.dict.seg_sum = c->comb_sum.p;
   E.dict.hperm = c->h_tiled ? c->hperm.p : nullptr;
   E.dict.cacc = 0;
+  E.dict.l2pf = 0;
   if (c->scatter == QPK_SCATTER_DICT && c->cacc) {
     E.dict.cacc = 1;
     E.dict.tile_beg = c->tile_beg.p; E.dict.cta_off = c->cta_off.p; E.dict.tslot = c->tslot.p;
     E.dict.cpart = c->cpart.p;
+    // long per-CTA tile streams (cfg4: ~380 tiles per CTA) gain from an L2
+    // prefetch 3 tiles beyond the ring (+3 %); short ones (cfg3: ~37) lose
+    // (A/B in DESIGN.md §4.3).  QPK_TILE_L2PF overrides.
+    const int per_cta = c->nblk / std::max(1, c->tile_grid);
+    E.dict.l2pf = per_cta >= 128 ? 3 : 0;
+    if (const char* ev = getenv("QPK_TILE_L2PF")) E.dict.l2pf = std::max(0, std::min(31, atoi(ev)));
     E.dict.col_ptr = c->col_ptr2.p; E.dict.col_pos = c->col_pos2.p;
     E.dict.comb_lanes = c->comb_lanes2; E.dict.nseg = c->comb_nseg2;
     E.dict.seg_beg = c->comb_beg2.p; E.dict.col_seg = c->comb_col2.p;

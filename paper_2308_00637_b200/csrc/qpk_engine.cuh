@@ -80,6 +80,7 @@ struct Dict {
   // partial per tile and column.
   const int* hperm;          // Hessian tiles: tile row q is H row hperm[q] (null: identity)
   int cacc;
+  int l2pf;                  // producer L2 prefetch distance in tiles (0 = off, < 32)
   const int* tile_beg;
   const int* cta_off;
   const int* tslot;

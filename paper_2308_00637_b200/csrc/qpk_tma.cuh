@@ -44,6 +44,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // tile descriptor written by the producer into its stage (visible to the
 // consumers through the mbarrier's release/acquire)
 struct TileDesc {
@@ -188,6 +192,17 @@ k_slot_rows_tile(Engine E, int par) {
       td.pad0 = __shfl_sync(0xffffffffu, cur_b.pad0, l);
       td.pad1 = __shfl_sync(0xffffffffu, cur_b.pad1, l);
       td.pad2 = __shfl_sync(0xffffffffu, cur_b.pad2, l);
+      if (D.l2pf) {
+        // L2 prefetch of the dense block D.l2pf tiles ahead (beyond the ring),
+        // so the stage's bulk copy is served from L2 when the stage frees
+        const int lp = l + D.l2pf;
+        const int pf_v0 = __shfl_sync(0xffffffffu, lp < 32 ? cur_b.v0 : nxt_b.v0, lp & 31);
+        const int pf_ra = __shfl_sync(0xffffffffu, lp < 32 ? cur_b.ra : nxt_b.ra, lp & 31);
+        const int pf_rb = __shfl_sync(0xffffffffu, lp < 32 ? cur_b.rb : nxt_b.rb, lp & 31);
+        const int pf_p = __shfl_sync(0xffffffffu, lp < 32 ? cur_b.pad0 : nxt_b.pad0, lp & 31);
+        if (lane == 0 && it + D.l2pf < my)
+          bulk_prefetch_l2(D.tval + pf_v0, round_up16((uint32_t)((pf_rb - pf_ra) * pf_p) * 8u));
+      }
       if (lane == 0) {
         const int s = it % QPK_TILE_STAGES;
         mbar_wait(&S.empty[s], ((it / QPK_TILE_STAGES) & 1) ^ 1);
