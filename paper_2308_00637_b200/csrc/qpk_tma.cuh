@@ -109,7 +109,6 @@ struct DTileSmem {
   double rpart[QPK_TILE_GROUPS][QPK_TILE_GWARPS][QPK_TILE_ROWS];
   alignas(16) double zs[QPK_TILE_GROUPS][QPK_TILE_ROWS];
   double red[32];
-  double s_lr[QPK_KMAX];
 };
 
 __device__ __forceinline__ void tile_group_bar(int g) {
