@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -611,6 +612,20 @@ static cudaError_t upload(DBuf<T>& dst, const std::vector<T>& src, cudaStream_t 
   return cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
 }
 
+// src followed by `pad` copies of `fill`, without a padded host copy of src
+// (pageable sources: the copies return once the host buffer is staged)
+template <typename T>
+static cudaError_t upload_padded(DBuf<T>& dst, const std::vector<T>& src, size_t pad, T fill, cudaStream_t s) {
+  cudaError_t e = dst.alloc(src.size() + pad);
+  if (e != cudaSuccess) return e;
+  if (!src.empty()) {
+    e = cudaMemcpyAsync(dst.p, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return e;
+  }
+  const std::vector<T> tail(pad, fill);
+  return cudaMemcpyAsync(dst.p + src.size(), tail.data(), pad * sizeof(T), cudaMemcpyHostToDevice, s);
+}
+
 #ifndef QPK_SYM_MIN_N
 #define QPK_SYM_MIN_N 512      // dense H at least this large is applied from packed symmetric tiles
 #endif
@@ -817,6 +832,17 @@ int qpk_problem_add_rows(qpk_ctx* c, int64_t n_rows, const int64_t* ro, const in
   const int64_t count = rows ? n_sel : n_rows;
   const long long mB = c->m_e + c->m_l + c->m_u;
   if (c->m + count > mB) return fail(QPK_E_ARG, "qpk_problem_add_rows: more rows than m_B=%lld", mB);
+  {
+    // one reservation for the whole call (rows padded to 4 entries)
+    size_t add = 0;
+    for (int64_t s = 0; s < count; ++s) {
+      const int64_t i = rows ? rows[s] : s;
+      if (i >= 0 && i < n_rows && ro[i + 1] >= ro[i]) add += (size_t)((ro[i + 1] - ro[i] + 3) & ~3LL);
+    }
+    c->h_ci.reserve(c->h_ci.size() + add);
+    c->h_v.reserve(c->h_v.size() + add);
+    c->h_rp.reserve(c->h_rp.size() + (size_t)count);
+  }
   for (int64_t s = 0; s < count; ++s) {
     const int64_t i = rows ? rows[s] : s;
     if (i < 0 || i >= n_rows) return fail(QPK_E_ARG, "qpk_problem_add_rows: row index %lld out of range", (long long)i);
@@ -1016,7 +1042,10 @@ static std::vector<int> rcm_order(long long n, const std::vector<int>& rp, const
 // Dense row tiles: consecutive rows grouped while (rows x padded distinct
 // columns) fits QPK_TILE_DOUBLES, each tile stored as a dense block over its
 // sorted column list.  have_dict = false when a single row is too wide.
-static int build_dict(qpk_ctx* c) {
+// probe = true (AUTO selection): give up after the first 64k rows when the
+// tiles come out sparse (random B: a tile is ~3 % nonzeros, and the full
+// dense-tile copy would be ~16 GB on cfg5 only to be rejected)
+static int build_dict(qpk_ctx* c, bool probe) {
   c->have_dict = false;
   c->h_tiled = false;
   const long long n = c->n, m = c->m;
@@ -1070,11 +1099,17 @@ static int build_dict(qpk_ctx* c) {
       slots += (r - ra) * pitch;
       tiles.push_back(td);
       ++tid;
+      if (probe && kind == 0 && !perm && ra < 65536 && r >= 65536 && r < nrows &&
+          (double)rp[r] < 0.3 * (double)slots) {
+        c->dict_reuse = (double)rp[r] / (double)slots;      // estimate from the probed rows
+        return -2;
+      }
     }
     return slots;
   };
+  tval.reserve(c->h_ci.size() + c->h_ci.size() / 4 + 64);
   const long long slots = tile_rows(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), m, 0, nullptr);
-  if (slots < 0) return QPK_OK;
+  if (slots < 0) return QPK_OK;                       // a row wider than a tile, or sparse tiles (probe)
   const size_t n_bcols = cols.size();
   const int n_btiles = tid;
   // the sparse Hessian's rows as dense tiles too (top-block rows, no B'z part),
@@ -1408,25 +1443,30 @@ static int build_cluster(qpk_ctx* c) {
   return QPK_OK;
 }
 
+// QPK_TIMING=1: host setup phases of qpk_problem_finalize on stderr
+struct SetupTimer {
+  bool on = getenv("QPK_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[qpk setup] %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 int qpk_problem_finalize(qpk_ctx* c, int scatter) {
+  SetupTimer tm;
   if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_finalize: no problem being built");
   const long long mB = c->m_e + c->m_l + c->m_u;
   if (c->m != mB) return fail(QPK_E_ARG, "qpk_problem_finalize: %lld rows added, m_B=%lld", c->m, mB);
   if (c->hkind < 0) return fail(QPK_E_STATE, "qpk_problem_finalize: Hessian not set");
   CUDA_TRY(cudaSetDevice(c->device));
   cudaStream_t s = c->stream;
-  {
-    // pad: the TMA tiles read aligned windows that may extend past the end
-    std::vector<int> rp = c->h_rp;
-    rp.resize(rp.size() + 16, rp.back());
-    CUDA_TRY(upload(c->rp, rp, s));
-    std::vector<int> ci = c->h_ci;
-    ci.resize(ci.size() + 32, -1);
-    CUDA_TRY(upload(c->ci, ci, s));
-    std::vector<double> bv = c->h_v;
-    bv.resize(bv.size() + 32, 0.0);
-    CUDA_TRY(upload(c->bv, bv, s));
-  }
+  // pad: the TMA tiles read aligned windows that may extend past the end
+  CUDA_TRY(upload_padded(c->rp, c->h_rp, 16, c->h_rp.back(), s));
+  CUDA_TRY(upload_padded(c->ci, c->h_ci, 32, -1, s));
+  CUDA_TRY(upload_padded(c->bv, c->h_v, 32, 0.0, s));
   if (c->hkind == QPK_HESS_DIAG || c->hkind == QPK_HESS_LOWRANK) CUDA_TRY(upload(c->hh, c->h_h, s));
   if (c->hkind == QPK_HESS_CSR) {
     CUDA_TRY(upload(c->hrp, c->h_hrp, s));
@@ -1459,6 +1499,7 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   CUDA_TRY(c->vin.alloc(N + 8));
   CUDA_TRY(c->zb.alloc(std::max<long long>(c->m, 1)));
 
+  tm.lap("upload");
   // lanes per row: ~3 chunks of 4 nonzeros per lane keeps several gathers in flight
   c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 12, 4, 32);
   if (const char* ev = getenv("QPK_LANES")) c->lanes = pow2_clamp(atoi(ev), 1, 32);
@@ -1485,16 +1526,20 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   c->scatter = QPK_SCATTER_ATOMIC;
   // a dense column panel (large systems in AUTO) comes first
   if (c->m > 0 && (scatter == QPK_SCATTER_PANEL || (scatter == QPK_SCATTER_AUTO && c->N() >= 50000))) {
+    tm.lap("row tiles");
     int rc = build_panel(c, scatter == QPK_SCATTER_PANEL);
     if (rc) return rc;
+    tm.lap("panel");
     if (c->have_panel) scatter = QPK_SCATTER_PANEL;
     else if (scatter == QPK_SCATTER_PANEL) scatter = QPK_SCATTER_CSC;     // no panel structure
   }
   if (scatter == QPK_SCATTER_PANEL) {
     c->scatter = QPK_SCATTER_PANEL;
   } else if ((scatter == QPK_SCATTER_AUTO || scatter == QPK_SCATTER_DICT) && c->m > 0) {
-    int rc = build_dict(c);
+    tm.lap("pre-dict");
+    int rc = build_dict(c, scatter == QPK_SCATTER_AUTO);
     if (rc) return rc;
+    tm.lap("dict");
     // Dense tiles pay off when they are mostly nonzeros (banded / clustered
     // B: RT, SVM, dense).  Such B makes fp64 atomics contend, so small
     // systems of that kind take the CSC gather (in the single-launch
@@ -1509,6 +1554,7 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     int rc = build_csc(c, c->h_rp, c->h_ci, c->h_v);
     if (rc) return rc;
     c->scatter = QPK_SCATTER_CSC;
+    tm.lap("csc");
   }
 
   // grid sizes: persistent kernel = all co-resident blocks (capped by work)
@@ -1593,6 +1639,7 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   std::vector<double>().swap(c->h_hv);
   c->building = false;
   c->finalized = true;
+  tm.lap("finish");
   return QPK_OK;
 }
 
