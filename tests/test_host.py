@@ -70,3 +70,38 @@ def test_oracle_operator_is_symmetric_positive_definite(rng):
         ku, kv = orc.apply_doubly_augmented(op, u), orc.apply_doubly_augmented(op, v)
         assert abs(u @ kv - v @ ku) <= 1e-10 * (1 + abs(u @ kv))
         assert v @ kv > 0
+
+
+def test_operator_cache_identity_and_content(monkeypatch):
+    """operator_for (direction.py): one device operator per live problem; the
+    same bound-index arrays skip hashing, equal contents in new arrays reuse
+    the operator, different bounds rebuild it (no device needed: GpuKkt is
+    stubbed)."""
+    from types import SimpleNamespace
+
+    from paper_2308_00637_b200 import direction
+
+    built = []
+
+    class FakeKkt:
+        def __init__(self, problem, bmap, device=0):
+            built.append(bmap)
+
+        def close(self):
+            pass
+
+    monkeypatch.setattr(direction, "GpuKkt", FakeKkt)
+    monkeypatch.setattr(direction, "_CACHE", {})
+    problem = SimpleNamespace()
+    lo, up = np.array([0, 2, 5]), np.array([1, 3])
+    op = SimpleNamespace(problem=problem, bmap=SimpleNamespace(lin_lower=lo, lin_upper=up))
+    gk = direction.operator_for(op)
+    assert direction.operator_for(op) is gk and len(built) == 1
+    key_fn = direction._bmap_key
+    monkeypatch.setattr(direction, "_bmap_key", lambda b: (_ for _ in ()).throw(AssertionError("hashed")))
+    assert direction.operator_for(op) is gk          # same array objects: no hashing
+    monkeypatch.setattr(direction, "_bmap_key", key_fn)
+    op2 = SimpleNamespace(problem=problem, bmap=SimpleNamespace(lin_lower=lo.copy(), lin_upper=up.copy()))
+    assert direction.operator_for(op2) is gk and len(built) == 1
+    op3 = SimpleNamespace(problem=problem, bmap=SimpleNamespace(lin_lower=np.array([0, 2]), lin_upper=up))
+    assert direction.operator_for(op3) is not gk and len(built) == 2
