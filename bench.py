@@ -6,18 +6,25 @@ density (B = -D_oar: 1.6e8 nnz, fp64), H = D_t'D_t (4.1e6 nnz) -- the largest
 configuration of BASELINE.json, the one it names for row sharding over
 1/2/4/8 GPUs and the one the north star's targets (>= 70 % of HBM bandwidth on
 1 GPU, >= 60 % efficiency at 8 GPUs on the largest sharded config) are stated
-on.  The operator is that of the first IPM iteration; one step = one direction
-solve = one call of the hot path: new diagonals (Jacobi rebuilt) + 200 PCG
-iterations from a seeded N(0,1) right-hand side (x0 = 0) + the final
-true-residual apply (linalg.py:132-133).  `--workload cfg1|cfg2|cfg3|cfg5`
+on.  The operator is that of the first IPM iteration; the Jacobi diagonal is
+built once before the timed loop in BOTH arms (its time is reported as
+`jacobi_ms`); one step = one PCG solve (linalg.py:66-133): 200 iterations
+(reference arm: 20, a bounded sample) from a seeded N(0,1) right-hand side
+(x0 = 0) + the final true-residual apply (linalg.py:132-133).  `--workload cfg1|cfg2|cfg3|cfg5`
 runs the other BASELINE configs the same way (cfg5 = the isolated operator
 sweep, 500 iterations); `--ipm` reports IPM wall time.  See DESIGN.md §5.
 
   value  PCG iterations/s, whole job, inputs resident in HBM
          (qpk_pcg_dev on device buffers), CUDA events on the solver's stream
   e2e    the same metric through the reference-facing drop-in
-         gpu_direction(op, rhs, cfg) with host buffers: diagonals + rhs H2D,
-         Jacobi build, PCG, solution D2H inside the timed region
+         gpu_direction(op, rhs, cfg) with the pageable numpy arrays the
+         reference IPM passes: diagonals + rhs H2D, Jacobi build, PCG,
+         solution D2H inside the timed region
+  parity the GPU's first iterations against the reference's on the same
+         operator and rhs (the cpu_baseline sample), printed in the line
+
+`--gpus N` without a torchrun environment re-launches itself under
+`python -m torch.distributed.run --nproc-per-node N` (one rank per GPU).
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -57,7 +64,9 @@ def parse():
                     help="0 = auto per matrix, 1 = atomic B'z, 2 = CSC gather, 3 = row-block dictionary")
     ap.add_argument("--cpu-iters", type=int, default=10, help="oracle iterations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-iters-per-step", type=int, default=5)
+    ap.add_argument("--ref-iters-per-step", type=int, default=20,
+                    help="PCG iterations per step of the reference arm (a bounded sample of the workload)")
+    ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--workload", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "svm_dual"],
                     help="cfg4 = headline (largest, sharded config); cfg1-4: PCG sweep on the first IPM iteration's "
                          "operator; cfg5: the isolated operator sweep")
@@ -124,9 +133,64 @@ def make_workload(name: str, scale: float, seed_offset: int = 0):
                                                                       + problem.m_eq)
     op = build_operator(problem, state)
     assert len(rhs) == op.dim
+    meta["state"] = state
     if name == "svm_dual":
         _SVM_META.update(meta)
     return problem, op, rhs, meta
+
+
+def config_of(args, meta):
+    """The `config` object -- identical in both arms (same workload, same seed)."""
+    return {"workload": WORKLOAD_DESC[args.workload] + (f" (scale {args.scale})" if args.scale != 1 else ""),
+            "seed": meta["seed"],
+            "l2": "inputs larger than L2 (every PCG iteration streams the whole operator)"
+                  if args.workload in ("cfg2", "cfg3", "cfg4", "cfg5", "svm_dual") and args.scale == 1 else
+                  "working set fits L2 (each step re-reads it every PCG iteration; no flush)"}
+
+
+class ReferencePath:
+    """The reference's CPU implementation of the path on one operator: the
+    UNMODIFIED qpipm from oracle/_ref (kind "reference") when it was placed by
+    build(), else the oracle port (kind "port", bit-identical on the goldens).
+    Jacobi is built once (timed apart); `run(k)` is linalg.pcg for k iterations
+    + the final true-residual apply, exactly what ipm._pcg_direction calls."""
+
+    def __init__(self, problem, op, meta, workload):
+        from oracle import build_ref
+        self.kind = "port"
+        if build_ref.available() and workload != "svm_dual":
+            from oracle import refbridge
+            qp = build_ref.import_qpipm()
+            rop = refbridge.ref_operator(problem, meta["state"])
+            assert np.array_equal(rop.d_diag, op.d_diag) and np.array_equal(rop.q_diag_extra, op.q_diag_extra)
+            self.kind = "reference"
+            self._pcg, self._cfg = qp.linalg.pcg, qp.linalg.PcgConfig
+            self._apply = lambda v: qp.kkt.apply_doubly_augmented(rop, v)      # noqa: E731
+            self._jacobi = lambda: qp.kkt.jacobi_diagonal(rop)                 # noqa: E731
+        else:
+            from oracle import qp_oracle as orc
+            hop = host_operator(op)
+            self._pcg, self._cfg = orc.pcg, orc.PcgConfig
+            self._apply = lambda v: orc.apply_doubly_augmented(hop, v)         # noqa: E731
+            self._jacobi = lambda: orc.jacobi_diagonal(hop)                    # noqa: E731
+        self._apply(np.zeros(op.dim))                 # warm the scipy views (not timed)
+        t0 = time.perf_counter()
+        self.jacobi = self._jacobi()
+        self.jacobi_s = time.perf_counter() - t0
+        self.inv = 1.0 / self.jacobi
+        self.cores = 1                                # numpy/scipy sparse matvecs are single-threaded
+
+    def apply(self, v):
+        return self._apply(v)
+
+    def run(self, rhs, iters, history=None):
+        cb = (lambda k, x, rn: history.append(rn)) if history is not None else None
+        return self._pcg(self._apply, lambda r: self.inv * r, rhs, self._cfg(tol=1e-300, max_iters=iters),
+                         callback=cb)
+
+    def describe(self):
+        return ("unmodified qpipm (oracle/_ref): linalg.pcg over kkt.apply_doubly_augmented" if self.kind == "reference"
+                else "oracle port (numpy/scipy restatement of qpipm, bit-identical on the golden vectors)")
 
 
 def algorithmic_bytes(op, iters: int, applies: int):
@@ -215,27 +279,28 @@ def host_operator(op, meta=None):
 _SVM_META = {}
 
 
-def cpu_baseline(op, rhs, iters: int, name: str = "cfg5"):
-    """The reference path (oracle restatement, bit-identical to qpipm on the
-    golden vectors) on a bounded sample: `iters` PCG iterations of cfg5."""
-    from oracle import qp_oracle as orc
-    op = host_operator(op)
-    orc.jacobi_diagonal(op)              # warm the scipy views (not timed)
+def cpu_baseline(ref, rhs, iters: int, name: str):
+    """The reference path on a bounded sample: `iters` PCG iterations (+ the
+    final apply) of the same operator and rhs.  Returns (record, history)."""
+    hist = []
     t0 = time.perf_counter()
-    res = orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=iters))
+    ref.run(rhs, iters, history=hist)
     dt = time.perf_counter() - t0
-    # iterations + the final true-residual apply, as in the GPU step
-    return {"value": iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{iters} PCG iterations of {name} (+ Jacobi build + final apply), {dt:.1f} s; "
-                      f"numpy/scipy oracle bit-identical to qpipm; sparse matvecs single-threaded "
-                      f"({len(os.sched_getaffinity(0))} host cores visible)"}
+    rec = {"value": iters / dt, "unit": UNIT, "cores": ref.cores, "kind": ref.kind,
+           "jacobi_build_s": round(ref.jacobi_s, 3),
+           "sample": f"{iters} PCG iterations of {name} + final apply, {dt:.1f} s (Jacobi built before, "
+                     f"{ref.jacobi_s:.1f} s); {ref.describe()}; sparse matvecs single-threaded "
+                     f"({len(os.sched_getaffinity(0))} host cores visible)"}
+    return rec, np.array([np.linalg.norm(rhs)] + hist)
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU path on the box's host cores,
+    same workload / metric / unit as our arm; rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    if args.workload == "svm_dual":
+    if args.workload == "svm_dual":               # Hessian on the host for the CPU arm (oracle restatement)
         from paper_2308_00637_b200.problem import build_operator
         from paper_2308_00637_b200.workloads import _state_from_initial, svm_dual_data
         from oracle import svm_oracle as so
@@ -246,25 +311,27 @@ def run_reference(args):
         meta = {"seed": 6}
     else:
         problem, op, rhs, meta = make_workload(args.workload, args.scale)
-    from oracle import qp_oracle as orc
+    ref = ReferencePath(problem, op, meta, args.workload)
     k_iter = args.ref_iters_per_step
-    orc.jacobi_diagonal(op)
     for _ in range(args.warmup):
-        orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=k_iter))
+        ref.run(rhs, k_iter)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        orc.pcg_direction(op, rhs, orc.PcgConfig(tol=1e-300, max_iters=k_iter))
+        res = ref.run(rhs, k_iter)
     dt = time.perf_counter() - t0
+    assert res.iterations == k_iter
     value = k_iter * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD_DESC[args.workload], "pcg_iters_per_step": k_iter,
-                   "seed": meta["seed"]},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port",
-                         "sample": f"{k_iter} PCG iterations per step of {args.workload} through the oracle "
-                                   f"(numpy/scipy restatement of qpipm, bit-identical on golden vectors)"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic (seeded generator of BASELINE.json configs[{CONFIG_INDEX[args.workload]}]; no dataset involved)",
+        "config": config_of(args, meta),
+        "step": {"pcg_iters_per_step": k_iter, "jacobi_ms": ref.jacobi_s * 1e3,
+                 "what": "one linalg.pcg call: k iterations + the final true-residual apply; Jacobi built once before"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": ref.cores, "kind": ref.kind,
+                         "sample": f"{k_iter} PCG iterations per step of {args.workload}; {ref.describe()}; "
+                                   f"{len(os.sched_getaffinity(0))} host cores visible, sparse matvecs single-threaded"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -306,10 +373,18 @@ def run_ours(args):
     x_d = torch.empty(len(rhs_loc), dtype=torch.float64, device=f"cuda:{local}")
     info = _native.PcgInfo()
 
-    def step():
-        # one IPM iteration's device work: new diagonals (marks the Jacobi
-        # diagonal stale -> rebuilt), then the fixed-iteration PCG solve
+    # Jacobi diagonal: built once, before the timed loop, in both arms
+    # (new diagonals mark it stale; qpk_jacobi rebuilds it); timed apart
+    jac_ms = []
+    for _ in range(3):
         gk.ctx.call("qpk_set_diagonals_dev", d_d.data_ptr(), q_d.data_ptr())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gk.jacobi()                                   # includes the D2H of the diagonal
+        jac_ms.append((time.perf_counter() - t0) * 1e3)
+
+    def step():
+        # one PCG solve (linalg.py:66-133): fixed iterations + the final true-residual apply
         gk.ctx.call("qpk_pcg_dev", rhs_d.data_ptr(), 1e-300, 1, args.iters, x_d.data_ptr(),
                     _native.ctypes.byref(info), None)
 
@@ -344,18 +419,9 @@ def run_ours(args):
     total_iters = args.iters * args.steps
     value = total_iters / elapsed
 
-    # e2e through the reference-facing drop-in, host buffers: the step's inputs
-    # (diagonals, rhs) live in pinned host memory, as a caller staging them
-    # for the GPU would keep them
-    import dataclasses
-
-    def pinned(a):
-        t = torch.empty(len(a), dtype=torch.float64, pin_memory=True)
-        out = t.numpy()
-        out[:] = a
-        return out
-    op = dataclasses.replace(op, d_diag=pinned(op.d_diag), q_diag_extra=pinned(op.q_diag_extra))
-    rhs = pinned(rhs)
+    # e2e through the reference-facing drop-in with the host buffers the
+    # reference IPM passes: plain (pageable) numpy arrays for the diagonals
+    # and the rhs (kkt.py:196-202, 242-262); the library stages them itself
     e2e_cfg = PcgConfig(tol=1e-300, max_iters=args.iters)
     if sharded_run:
         from paper_2308_00637_b200.sharded import sharded_direction
@@ -380,7 +446,7 @@ def run_ours(args):
     h2d = 8 * (len(d_loc) + op.n + len(rhs_loc))     # per rank: its diagonals + rhs slice
     d2h = 8 * len(rhs_loc)
 
-    # roofline of the dominant kernel (the persistent PCG kernel: one launch per step)
+    # roofline: ALGORITHMIC bytes per launch (one launch = one solve) / its device time
     per_launch, per_iter = algorithmic_bytes(op, args.iters, applies=1)
     avg_ms = float(np.mean(kernel_ms))
     achieved = per_launch / world / (avg_ms * 1e-3) / 1e9     # per GPU
@@ -392,41 +458,46 @@ def run_ours(args):
         try:
             rec = json.loads(prof.read_text()).get(args.workload)
             if rec and args.scale == 1.0 and world == 1:
-                # ncu DRAM bytes of the same solve (per-iteration figure x iterations + final apply)
+                # ncu DRAM bytes of the same solve (per-iteration figure x iterations + final apply),
+                # captured once per build by probes/ncu_traffic.py -- not measured in this run
                 traffic = float(rec["dram_bytes_per_iter"]) * (args.iters + 1)
                 traffic_src = rec.get("source")
         except Exception:
             traffic = None
-    # the pass over B (dominant kernel of a PCG iteration): matrix bytes / its time
+    # PHYSICAL bandwidth: the bytes the kernels really moved (ncu DRAM) / the same time
+    physical = traffic / (avg_ms * 1e-3) / 1e9 if traffic else None
+    # the pass over B (dominant kernel of a PCG iteration): its time, and the
+    # bytes of the format it streams (tile / panel formats hold fewer bytes than CSR)
     phases = np.mean(phase_ms, axis=0) * 1e3 / args.iters          # us per iteration
     rows_kernel = {3: "k_slot_rows_tile", 4: "k_slot_panel"}.get(gk.ctx.query("scatter"), "k_slot_rows") \
         if engine_used else "pcg_kernel (rows phase)"
-    mat_bytes = per_iter - 88 * op.dim
+    fmt_bytes = gk.ctx.query("format_bytes")
     dom = {"name": rows_kernel, "us_per_iter": round(float(phases[1]), 2),
            "share_of_iteration": round(float(phases[1] / max(phases.sum(), 1e-9)), 3),
-           "matrix_bytes_per_iter": mat_bytes,
-           "achieved_matrix_GBs": round(mat_bytes / world / (phases[1] * 1e-6) / 1e9, 1) if phases[1] > 0 else None}
+           "csr_matrix_bytes_per_iter": per_iter - 88 * op.dim,
+           "format_bytes_per_pass": fmt_bytes,
+           "format_GBs": round(fmt_bytes / (phases[1] * 1e-6) / 1e9, 1) if phases[1] > 0 and fmt_bytes > 0 else None}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic (seeded generator of BASELINE.json configs[{CONFIG_INDEX[args.workload]}]; no dataset involved)",
-            "config": {"workload": WORKLOAD_DESC[args.workload] + (f" (scale {args.scale})" if args.scale != 1 else "")
-                                   + f"; {args.iters} PCG iterations per step (+ Jacobi build + final apply)",
-                       "parallelism": f"rowshard{world} (NCCL all-reduce per iteration)" if world > 1 else "single",
+            "config": config_of(args, meta),
+            "step": {"pcg_iters_per_step": args.iters, "jacobi_ms": round(float(np.median(jac_ms)), 3),
+                     "what": "one PCG solve: k iterations + the final true-residual apply; Jacobi built once before "
+                             "(jacobi_ms = build + D2H of the diagonal)"},
+            "engine": {"parallelism": f"rowshard{world} (NCCL all-reduce per iteration)" if world > 1 else "single",
                        "scatter": {1: "atomic", 2: "csc", 3: "dict", 4: "panel"}.get(gk.ctx.query("scatter"), "?"),
-                       "l2": "inputs larger than L2" if per_iter > 126e6 else
-                       "working set fits L2 (each step re-reads it every PCG iteration; no flush)",
                        "n": op.n, "m_B": op.m, "nnz_B": gk.ctx.query("nnz"),
                        "grid": gk.ctx.query("grid"), "lanes_per_row": gk.ctx.query("lanes"),
                        "hess_tiled": gk.ctx.query("hess_tiled"), "tile_cta_acc": gk.ctx.query("tile_cta_acc"),
                        "panel_cols": gk.ctx.query("panel_cols"),
-                       "engine": "slot engine (per-phase kernels, CUDA graph)" if engine_used else
-                                 "persistent cooperative kernel",
-                       "seed": meta["seed"]},
+                       "kind": "slot engine (per-phase kernels, CUDA graph)" if engine_used else
+                               ("one thread-block cluster" if gk.ctx.query("cluster") else "persistent cooperative kernel")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "physical_GBs": physical, "physical_frac": physical / peak if physical else None,
                          "algorithmic_bytes_per_launch": per_launch, "algorithmic_bytes_per_iter": per_iter,
                          "kernel": (f"slot engine: {rows_kernel} + top / combine / update kernels per iteration "
                                     "(achieved = the whole solve's algorithmic bytes / its device time)"
@@ -440,7 +511,8 @@ def run_ours(args):
                                                        [round(v * 1e3 / args.iters, 2) for v in np.mean(phase_ms, axis=0)])),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "gpu_direction(op, rhs, PcgConfig) host buffers"},
+                    "path": "gpu_direction(op, rhs, PcgConfig): pageable numpy inputs as the reference IPM passes them; "
+                            "diagonals + rhs H2D, Jacobi build, PCG, solution D2H"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
@@ -458,7 +530,22 @@ def run_ours(args):
                 "frac": round(floor_us / float(phases[1]), 3),
                 "source": "profiles/r01_probe_random_access2.txt (8 MB table, 148 SMs)"}
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(op, rhs, args.cpu_iters, args.workload)
+            # the reference on the same operator and rhs: the CPU baseline AND the
+            # parity check of this very run (first iterations of the benchmarked path)
+            ref = ReferencePath(problem, op, meta, args.workload)
+            line["cpu_baseline"], ref_hist = cpu_baseline(ref, rhs, args.cpu_iters, args.workload)
+            v = np.random.default_rng(1234).standard_normal(op.dim)
+            y_ref = ref.apply(v)
+            gk2 = operator_for(op, device=local)
+            gk2.set_diagonals(op.d_diag, op.q_diag_extra)
+            apply_err = float(np.linalg.norm(gk2.apply(v) - y_ref) / np.linalg.norm(y_ref))
+            jac_err = float(np.max(np.abs(gk2.jacobi() - ref.jacobi) / np.abs(ref.jacobi)))
+            _, ginfo, ghist = gk2.pcg(rhs, 1e-300, args.cpu_iters, True, history=True)
+            hist_dev = float(np.max(np.abs(ghist - ref_hist) / ref_hist))
+            line["parity"] = {"apply_rel_err": apply_err, "jacobi_rel_err": jac_err, "hist_dev": hist_dev,
+                              "iterations_compared": int(ginfo.iterations), "against": ref.kind,
+                              "ok": bool(apply_err <= 1e-12 and jac_err <= 1e-12 and hist_dev <= 1e-8),
+                              "gates": "apply, Jacobi <= 1e-12 relative; residual history <= 1e-8 relative"}
         print(json.dumps(line), flush=True)
     gk.close()
     if world > 1 or args.force_sharded:
@@ -542,8 +629,29 @@ def run_ipm(args):
     print(json.dumps(line), flush=True)
 
 
+def relaunch_under_torchrun(args):
+    """`python bench.py --gpus N` outside torchrun: re-launch as N ranks, one per
+    GPU, exactly as the driver would (127.0.0.1 rendezvous on a free port)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *sys.argv[1:]]
+    raise SystemExit(subprocess.run(cmd).returncode)
+
+
 def main():
     args = parse()
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.ipm:
+        relaunch_under_torchrun(args)
+    if args.launch_check:                 # launcher test (CPU): what each rank sees
+        rank, world, local = dist_env()
+        print(json.dumps({"launch_check": True, "rank": rank, "world": world, "local_rank": local,
+                          "gpus": args.gpus}), flush=True)
+        return
+    if args.impl == "ours" and not args.ipm and dist_env()[1] != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={dist_env()[1]}")
     if args.ipm and args.impl != "reference":
         run_ipm(args)
         return

@@ -308,6 +308,20 @@ __global__ void __launch_bounds__(256) k_pack_sym(const double* __restrict__ Hd,
   }
 }
 
+// H == H' bit for bit?  (the packed upper-tile apply mirrors the upper triangle;
+// the reference's hessian_apply, model.py:165-176, multiplies whatever it is given)
+__global__ void __launch_bounds__(256) k_sym_check(const double* __restrict__ Hd, long long n, int* __restrict__ bad) {
+  const int I = blockIdx.y, J = blockIdx.x;
+  if (J < I) return;
+  int mism = 0;
+  for (int e = threadIdx.x; e < 4096; e += 256) {
+    const long long r = (long long)I * 64 + e / 64, col = (long long)J * 64 + e % 64;
+    if (r < n && col < n && col > r)
+      mism |= __double_as_longlong(Hd[r * n + col]) != __double_as_longlong(Hd[col * n + r]);
+  }
+  if (mism) atomicOr(bad, 1);
+}
+
 __global__ void __launch_bounds__(QPK_BLOCK) k_prep(Op op, const double* v, double* y, double* part, int G) {
   __shared__ double red[32];
   phase_prep(op, v, y, part, G, red);
@@ -521,6 +535,7 @@ struct qpk_ctx {
   // CTA-level accumulation of the tile partials (Dict::cacc)
   bool cacc = false;
   int tile_grid = 0;
+  bool h_symmetric = true;
   DBuf<int> tile_beg, cta_off, tslot, col_ptr2, col_pos2, comb_beg2, comb_col2;
   DBuf<double> cpart;
   int comb_lanes2 = 8, comb_nseg2 = 0, comb_max2 = 0;   // max CTA partials of one column
@@ -585,9 +600,11 @@ struct qpk_ctx {
   DBuf<EngineCfg> ecfg;
   int* pinned_mode = nullptr;    // [2] host-mapped poll flags
   cudaEvent_t poll_ev[2] = {nullptr, nullptr};
+  cudaEvent_t time_ev[2] = {nullptr, nullptr};   // solve timing (created once, reused)
   cudaGraphExec_t graph = nullptr;
   int graph_slots = 0;
   bool graph_failed = false;
+  int attr_scatter = -1, attr_kp = -1;
 
   Op op() const {
     Op o;
@@ -769,6 +786,7 @@ int qpk_destroy(qpk_ctx* c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
   if (c->comm && nccl().ok) nccl().commDestroy(c->comm);
   for (auto& e : c->poll_ev) if (e) cudaEventDestroy(e);
+  for (auto& e : c->time_ev) if (e) cudaEventDestroy(e);
   if (c->pinned_mode) cudaFreeHost(c->pinned_mode);
   if (c->own) cudaStreamDestroy(c->own);
   delete c;
@@ -818,6 +836,7 @@ int qpk_problem_begin(qpk_ctx* c, int64_t n, int64_t m_e, int64_t m_l, int64_t m
                 (long long)m_e, (long long)m_l, (long long)m_u);
   if (n + m_e + m_l + m_u >= (1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "dimension exceeds int32 range");
   c->building = true; c->finalized = false; c->diag_set = false; c->jac_ready = false; c->have_csc = false;
+  c->graph_failed = false; c->h_symmetric = true;
   c->n = n; c->m_e = m_e; c->m_l = m_l; c->m_u = m_u; c->m = 0;
   c->h_rp.assign(1, 0); c->h_ci.clear(); c->h_v.clear(); c->nnz = 0;
   c->hkind = -1; c->hk = 0;
@@ -1164,7 +1183,10 @@ static int build_dict(qpk_ctx* c, bool probe) {
   // memory; the combine then reads ~one partial per (CTA, column)
   c->cacc = false;
   if (!getenv("QPK_NO_CACC")) {
-    const int G = std::max(1, std::min(c->sms, tid));
+    int G = std::max(1, std::min(c->sms, tid));
+    // test switch: fewer CTAs -> long per-CTA tile streams on small problems
+    // (ring-stage reuse, descriptor refill, L2 prefetch; tests/test_gpu_fullscale.py)
+    if (const char* ev = getenv("QPK_TILE_GRID")) G = std::max(1, std::min(G, atoi(ev)));
     std::vector<long long> pre(tid + 1, 0);
     // weight = dense slots + a fixed per-tile cost (barriers, copies) of ~2k slots
     for (int t = 0; t < tid; ++t) pre[t + 1] = pre[t] + (long long)(tiles[t].rb - tiles[t].ra) * tiles[t].pad0 + 2048;
@@ -1594,6 +1616,22 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   if (c->hkind == QPK_HESS_DENSE && c->cl_C == 0 && !c->sharded && c->n >= QPK_SYM_MIN_N && !getenv("QPK_NO_SYM")) {
     const int nt = (int)((c->n + 63) / 64);
     const size_t tiles = (size_t)nt * (nt + 1) / 2;
+    // only a bitwise symmetric H may be packed; any other DenseHessian keeps
+    // the row-major apply (h.m @ v for whatever m is, as the reference)
+    DBuf<int> bad;
+    CUDA_TRY(bad.alloc(1));
+    CUDA_TRY(cudaMemsetAsync(bad.p, 0, sizeof(int), s));
+    k_sym_check<<<dim3(nt, nt), 256, 0, s>>>(c->hdense.p, c->n, bad.p);
+    c->launches++;
+    int h_bad = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->h_symmetric = h_bad == 0;
+  }
+  if (c->hkind == QPK_HESS_DENSE && c->cl_C == 0 && !c->sharded && c->n >= QPK_SYM_MIN_N && !getenv("QPK_NO_SYM") &&
+      c->h_symmetric) {
+    const int nt = (int)((c->n + 63) / 64);
+    const size_t tiles = (size_t)nt * (nt + 1) / 2;
     CUDA_TRY(c->hsym.alloc(tiles * 4096));
     k_pack_sym<<<dim3(nt, nt), 256, 0, s>>>(c->hdense.p, c->n, nt, c->hsym.p);
     c->launches++;
@@ -2019,9 +2057,14 @@ static Engine make_engine(qpk_ctx* c) {
 }
 
 static int engine_setup(qpk_ctx* c) {
+  // per-format kernel attributes: a context may be re-finalized with another
+  // problem (qpk_problem_begin again), so these are set for the current format
+  if (c->attr_scatter != c->scatter || c->attr_kp != c->panel_kp) {
+    CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem()));
+    if (c->scatter == QPK_SCATTER_PANEL) CUDA_TRY(panel_attr(c));
+    c->attr_scatter = c->scatter; c->attr_kp = c->panel_kp;
+  }
   if (c->ctrl.p) return QPK_OK;
-  CUDA_TRY(cudaFuncSetAttribute(k_slot_rows_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem()));
-  if (c->scatter == QPK_SCATTER_PANEL) CUDA_TRY(panel_attr(c));
   CUDA_TRY(c->ctrl.alloc(2));
   CUDA_TRY(c->gscal.alloc(4));
   CUDA_TRY(c->lscal2.alloc(2));
@@ -2129,9 +2172,8 @@ static int pcg_impl(qpk_ctx* c, const double* rhs_dev, double tol, int rel, int6
   if (!c->jac_ready) { int rc = build_jacobi(c); if (rc) return rc; }
   if (rhs_dev != c->rhs.p)
     CUDA_TRY(cudaMemcpyAsync(c->rhs.p, rhs_dev, c->N() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-  cudaEvent_t e0, e1;
-  CUDA_TRY(cudaEventCreate(&e0));
-  CUDA_TRY(cudaEventCreate(&e1));
+  for (auto& e : c->time_ev) if (!e) CUDA_TRY(cudaEventCreate(&e));
+  cudaEvent_t e0 = c->time_ev[0], e1 = c->time_ev[1];
   CUDA_TRY(cudaEventRecord(e0, c->stream));
   PcgOut o;
   if (use_engine(c)) {
@@ -2177,8 +2219,6 @@ static int pcg_impl(qpk_ctx* c, const double* rhs_dev, double tol, int rel, int6
   CUDA_TRY(cudaStreamSynchronize(c->stream));
   float ms = 0.f;
   CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   const double* res = c->x[o.result_buf].p;
   CUDA_TRY(cudaMemcpyAsync(x_dev, res, c->N() * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
   if (info) {
@@ -2476,9 +2516,21 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
   if (k == "tile_density_x100") return (int64_t)(c->dict_reuse * 100);
   if (k == "hess_tiled") return c->h_tiled ? 1 : 0;
   if (k == "hess_sym") return c->h_nchunks > 0 ? 1 : 0;
+  if (k == "hess_symmetric") return c->h_symmetric ? 1 : 0;
   if (k == "dense_rows") return c->n_dense;
   if (k == "cluster") return c->cl_C;
   if (k == "tile_cta_acc") return c->cacc ? 1 : 0;
+  if (k == "tile_grid") return c->tile_grid;
+  if (k == "format_bytes") {
+    // bytes of the chosen apply format that one pass over B (and a tiled H) streams
+    if (c->scatter == QPK_SCATTER_DICT)
+      return (int64_t)(c->tval.bytes() + c->dcols.bytes() + (c->cacc ? c->tslot.bytes() : 0) + c->tiles.bytes());
+    if (c->scatter == QPK_SCATTER_PANEL)
+      return (int64_t)(c->panel_P.bytes() + c->panel_ev.bytes() + c->panel_eci.bytes());
+    const int64_t csr = (int64_t)(c->ci.bytes() + c->bv.bytes() + c->rp.bytes());
+    return c->scatter == QPK_SCATTER_CSC ? csr + (int64_t)(c->ri.bytes() + c->cv.bytes() + c->cp.bytes()) : csr;
+  }
+  if (k == "tile_l2pf") return (c->scatter == QPK_SCATTER_DICT && c->cacc) ? make_engine(c).dict.l2pf : 0;
   if (k == "panel_kp") return c->panel_kp;
   if (k == "panel_cols") return c->panel_kd;
   if (k == "panel_ew") return c->panel_ew;

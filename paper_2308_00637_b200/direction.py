@@ -75,7 +75,9 @@ class GpuKkt:
             c.call("qpk_set_hessian_csr", _native.ptr(ro), _native.ptr(ci), _native.ptr(v))
         elif kind == "DenseHessian":
             mm = np.ascontiguousarray(h.m, dtype=np.float64)
-            _dim(mm.shape[0], self.n, "Hessian")
+            if mm.ndim != 2 or mm.shape != (self.n, self.n):
+                from .problem import DimensionError
+                raise DimensionError(f"dense Hessian has shape {mm.shape}, expected {(self.n, self.n)}")
             c.call("qpk_set_hessian_dense", _native.ptr(mm))
         elif kind == "DeviceDenseHessian":             # SVM dual: built on the device (svm.py)
             _dim(h.n, self.n, "Hessian")

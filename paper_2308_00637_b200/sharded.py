@@ -79,7 +79,8 @@ class ShardedKkt:
         segs = b_row_segments(problem, bmap)
         self.m = int(sum(len(r) if r is not None else m.n_rows for m, r, _ in segs))
         self.dim = self.n + self.m
-        self.lo, self.hi = partition_rows(b_row_nnz(segs), self.world)[self.rank]
+        self.bounds = partition_rows(b_row_nnz(segs), self.world)
+        self.lo, self.hi = self.bounds[self.rank]
         self.ctx = _native.Context(device)
         lib = _native.load_library()
         uid = (ctypes.c_ubyte * 128)()
@@ -122,11 +123,22 @@ class ShardedKkt:
         return np.ascontiguousarray(np.concatenate([v[:self.n], v[self.n + self.lo:self.n + self.hi]]))
 
     def gather(self, v_loc):
-        """Global vector from the ranks' (replicated top, local bottom) pieces."""
+        """Global vector from the ranks' (replicated top, local bottom) pieces:
+        one all_gather of equal-sized (padded) tensors on the group's backend
+        (device tensors under NCCL, host tensors under gloo)."""
+        import torch
         dist = _dist()
-        parts = [None] * self.world
-        dist.all_gather_object(parts, v_loc[self.n:], group=self.group)
-        return np.concatenate([v_loc[:self.n]] + list(parts))
+        sizes = [hi - lo for lo, hi in self.bounds]
+        width = max(max(sizes), 1)
+        on_gpu = dist.get_backend(self.group) == "nccl"
+        piece = torch.zeros(width, dtype=torch.float64)
+        piece[:sizes[self.rank]] = torch.from_numpy(np.ascontiguousarray(v_loc[self.n:]))
+        if on_gpu:
+            piece = piece.to(f"cuda:{self.ctx.device}")
+        out = torch.empty(self.world * width, dtype=torch.float64, device=piece.device)
+        dist.all_gather_into_tensor(out, piece, group=self.group)
+        out = out.cpu().numpy().reshape(self.world, width)
+        return np.concatenate([v_loc[:self.n]] + [out[r, :sizes[r]] for r in range(self.world)])
 
     def jacobi(self):
         out = np.empty(self.n + self.hi - self.lo)
@@ -158,16 +170,27 @@ _CACHE: dict = {}
 
 
 def sharded_direction(op, rhs, cfg, device: int | None = None, group=None):
-    """DirectionSolver for an SPMD caller (all ranks, same op and rhs)."""
+    """DirectionSolver for an SPMD caller (all ranks, same op and rhs).  The
+    device operator is cached per (problem, bound map), as direction.operator_for
+    does; a replaced entry is closed at once -- on every rank at the same call,
+    so the NCCL communicators are destroyed in the same order everywhere."""
+    from .direction import _bmap_key
     PcgResult, PcgBreakdownError = result_types()
     key = id(op.problem)
     entry = _CACHE.get(key)
-    if entry is None or entry[0] is not op.problem:
+    fresh = entry is None or entry[0] is not op.problem
+    if not fresh:
+        same = entry[3][0] is op.bmap.lin_lower and entry[3][1] is op.bmap.lin_upper
+        fresh = not (same or entry[2] == _bmap_key(op.bmap))
+    if fresh:
         if device is None:
             import torch
             device = torch.cuda.current_device()
-        entry = (op.problem, ShardedKkt(op.problem, op.bmap, device=device, group=group))
+        for old in list(_CACHE.values()):
+            old[1].close()
         _CACHE.clear()
+        entry = (op.problem, ShardedKkt(op.problem, op.bmap, device=device, group=group), _bmap_key(op.bmap),
+                 (op.bmap.lin_lower, op.bmap.lin_upper))
         _CACHE[key] = entry
     sk = entry[1]
     sk.set_diagonals(op.d_diag, op.q_diag_extra)
