@@ -2045,8 +2045,9 @@ static Engine make_engine(qpk_ctx* c) {
     // long per-CTA tile streams (cfg4: ~380 tiles per CTA) gain from an L2
     // prefetch 3 tiles beyond the ring (+3 %); short ones (cfg3: ~37) lose
     // (A/B in DESIGN.md §4.3).  QPK_TILE_L2PF overrides.
-    const int per_cta = c->nblk / std::max(1, c->tile_grid);
-    E.dict.l2pf = per_cta >= 128 ? 3 : 0;
+    // (with the evict-first stream the prefetch no longer pays: cfg4 297 us
+    // without it, 307 us with 3 tiles; kept as a switch)
+    E.dict.l2pf = 0;
     if (const char* ev = getenv("QPK_TILE_L2PF")) E.dict.l2pf = std::max(0, std::min(31, atoi(ev)));
     E.dict.col_ptr = c->col_ptr2.p; E.dict.col_pos = c->col_pos2.p;
     E.dict.comb_lanes = c->comb_lanes2; E.dict.nseg = c->comb_nseg2;

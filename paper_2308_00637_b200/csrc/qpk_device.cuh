@@ -64,15 +64,33 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // ---------------------------------------------------------------- loads ----
+// Streaming loads of matrix data (read once per pass, far larger than L2):
+// no L1 allocation and an L2 evict-first policy, so the stream does not flush
+// the vectors (u, y, z, ...) the same pass gathers from and scatters into.
+__device__ __forceinline__ unsigned long long stream_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));   // pure: hoisted out of loops
+  return pol;
+}
 __device__ __forceinline__ int4 ld_stream_i4(const int* p) {
   int4 r;
+#ifndef QPK_NO_STREAM_HINT
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p), "l"(stream_policy()));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+#endif
   return r;
 }
 __device__ __forceinline__ double2 ld_stream_d2(const double* p) {
   double2 r;
+#ifndef QPK_NO_STREAM_HINT
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(stream_policy()));
+#else
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+#endif
   return r;
 }
 

@@ -137,6 +137,7 @@ __global__ void __launch_bounds__(QPK_PANEL_CW * 32, 1) k_slot_panel(Engine E, i
   // producer: lane 0 of warp 0 issues chunk `it` into stage it % S once the
   // stage's previous chunk has been consumed by every warp
   const bool ldx = fuse && c.xupd;
+  const unsigned long long pol = l2_evict_first_policy();
   auto produce = [&](int it) {
     if (it >= nch) return;
     const int s = it % S;
@@ -158,7 +159,11 @@ __global__ void __launch_bounds__(QPK_PANEL_CW * 32, 1) k_slot_panel(Engine E, i
       }
     }
     mbar_expect_tx(&full[s], b_p + b_d + b_w + (fuse ? b_w : 0u) + (ldx ? b_w : 0u) + (direct ? 2u : 1u) * b_e + b_ec);
+#ifndef QPK_NO_STREAM_HINT
+    bulk_g2s_stream(st, P.P + (size_t)r0 * kp, b_p, &full[s], pol);   // the panel is streamed once per pass
+#else
     bulk_g2s(st, P.P + (size_t)r0 * kp, b_p, &full[s]);
+#endif
     bulk_g2s(st + L.o_d, op.d + v0, b_d, &full[s]);
     bulk_g2s(st + L.o_w, v + w0, b_w, &full[s]);
     if (fuse) bulk_g2s(st + L.o_r, E.r + w0, b_w, &full[s]);

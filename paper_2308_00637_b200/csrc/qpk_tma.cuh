@@ -44,6 +44,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+// the same copy with an L2 evict-first policy: data streamed once per pass
+__device__ __forceinline__ void bulk_g2s_stream(void* dst, const void* src, uint32_t bytes, unsigned long long* bar,
+                                                unsigned long long policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -168,6 +183,17 @@ k_slot_rows_tile(Engine E, int par) {
     // dependent descriptor load sits between a stage's release and its refill.
     const double* wsrc = v;
     const double* xsrc = E.x[c.cur];
+    // The dense blocks are streamed once per pass (1.4 GB on cfg4, far beyond
+    // L2): an L2 evict-first policy on their copies keeps the vectors the
+    // slot's kernels re-read (p, r, x, y, d: ~14 MB each) resident instead of
+    // being flushed by the stream (A/B: cfg4 tile pass 318 -> 297 us, cfg3 42.9 -> 39.5 us)
+#ifndef QPK_TILE_NO_EVICT_FIRST
+    const unsigned long long pol = l2_evict_first_policy();
+#define TILE_A_COPY(dst, src, bytes, bar) bulk_g2s_stream(dst, src, bytes, bar, pol)
+#else
+#define TILE_A_COPY(dst, src, bytes, bar) bulk_g2s(dst, src, bytes, bar)
+#endif
+#define TILE_C_COPY(dst, src, bytes, bar) bulk_g2s(dst, src, bytes, bar)
     auto ld_desc = [&](int base) {
       int4 lo = make_int4(0, 0, 0, 0), hi = lo;
       const int k = base + lane;
@@ -216,15 +242,15 @@ k_slot_rows_tile(Engine E, int par) {
           // (its row ids hperm[ra .. rb) land in st.d, from a 16-byte aligned start)
           const uint32_t b_j = D.hperm ? round_up16((uint32_t)(td.rb - (td.ra & ~3)) * 4u) : 0u;
           mbar_expect_tx(&S.full[s], b_a + b_c + b_j);
-          bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
-          bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
+          TILE_A_COPY(st.a, D.tval + td.v0, b_a, &S.full[s]);
+          TILE_C_COPY(st.cols, D.cols + td.d0, b_c, &S.full[s]);
           if (b_j) bulk_g2s(st.d, D.hperm + (td.ra & ~3), b_j, &S.full[s]);
         } else {
           const uint32_t b_d = round_up16((uint32_t)(((td.rb + 1) & ~1) - v0) * 8u);
           const uint32_t b_w = round_up16((uint32_t)(((op.n + td.rb + 1) & ~1) - w0) * 8u);
           mbar_expect_tx(&S.full[s], b_a + b_c + b_d + b_w + (fuse ? 2 * b_w : 0u));
-          bulk_g2s(st.a, D.tval + td.v0, b_a, &S.full[s]);
-          bulk_g2s(st.cols, D.cols + td.d0, b_c, &S.full[s]);
+          TILE_A_COPY(st.a, D.tval + td.v0, b_a, &S.full[s]);
+          TILE_C_COPY(st.cols, D.cols + td.d0, b_c, &S.full[s]);
           bulk_g2s(st.d, op.d + v0, b_d, &S.full[s]);
           bulk_g2s(st.w, wsrc + w0, b_w, &S.full[s]);
           if (fuse) {
@@ -378,6 +404,19 @@ k_slot_rows_tile(Engine E, int par) {
       for (int cc = tid; cc < nd; cc += T) {
         double s0 = 0.0, s1 = 0.0;
         int rr = 0;
+#ifndef QPK_TILE_NO_COLUNROLL
+        {
+          const double* ac = st.a + cc;
+          const double* zz = S.zs[g];
+          for (; rr + 7 < R; rr += 8) {
+            double av[8], zv[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) { av[q] = ac[(rr + q) * pitch]; zv[q] = zz[rr + q]; }
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) { s0 = fma(av[q], zv[q], s0); s1 = fma(av[q + 1], zv[q + 1], s1); }
+          }
+        }
+#endif
         for (; rr + 1 < R; rr += 2) {
           s0 = fma(st.a[rr * pitch + cc], S.zs[g][rr], s0);
           s1 = fma(st.a[(rr + 1) * pitch + cc], S.zs[g][rr + 1], s1);
