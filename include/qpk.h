@@ -113,6 +113,38 @@ int qpk_synchronize(qpk_ctx* ctx);
 int qpk_nccl_get_unique_id(unsigned char id[128]);
 int qpk_shard_init(qpk_ctx* ctx, int world, int rank, const unsigned char id[128]);
 
+/* ---- multi-GPU from ONE process (the reference's solve() is a single
+ * process, ipm.py:185-206) ----------------------------------------------------
+ * qpk_multi owns one context per listed device, shards B by rows over them
+ * (contiguous, nnz-balanced blocks, as the one-process-per-GPU layout) and
+ * runs every call on one host thread per device; the per-iteration
+ * all-reduces go through one NCCL communicator per device.  All vectors are
+ * GLOBAL host vectors (d: m_B, q: n, v / rhs / x: n + m_B).  The arrays given
+ * to qpk_multi_problem_add_rows / qpk_multi_set_hessian_* are read at
+ * qpk_multi_problem_finalize and must stay valid until it returns. */
+typedef struct qpk_multi qpk_multi;
+int qpk_multi_create(int n_devices, const int* device_ids, qpk_multi** out);
+int qpk_multi_destroy(qpk_multi* mm);
+int qpk_multi_devices(qpk_multi* mm);
+qpk_ctx* qpk_multi_context(qpk_multi* mm, int rank);
+int qpk_multi_problem_begin(qpk_multi* mm, int64_t n, int64_t m_e, int64_t m_l, int64_t m_u);
+int qpk_multi_problem_add_rows(qpk_multi* mm, int64_t n_rows, const int64_t* row_offsets,
+                               const int64_t* col_indices, const double* values,
+                               const int64_t* rows, int64_t n_sel, double sign);
+int qpk_multi_set_hessian_diag(qpk_multi* mm, const double* d);
+int qpk_multi_set_hessian_csr(qpk_multi* mm, const int64_t* row_offsets, const int64_t* col_indices,
+                              const double* values);
+int qpk_multi_set_hessian_dense(qpk_multi* mm, const double* m_rowmajor);
+int qpk_multi_set_hessian_lowrank(qpk_multi* mm, const double* h0, int64_t k, const double* u_rowmajor,
+                                  const double* w);
+int qpk_multi_problem_finalize(qpk_multi* mm, int scatter);
+int qpk_multi_set_diagonals(qpk_multi* mm, const double* d_diag, const double* q_diag_extra);
+int qpk_multi_jacobi(qpk_multi* mm, double* diag_out);
+int qpk_multi_apply(qpk_multi* mm, const double* v, double* y);
+int qpk_multi_pcg(qpk_multi* mm, const double* rhs, double tol, int tol_is_relative, int64_t max_iters,
+                  double* x_out, qpk_pcg_info* info, double* resid_hist);
+int64_t qpk_multi_query(qpk_multi* mm, int rank, const char* key);
+
 /* ---- problem upload (once per QpProblem) ------------------------------ */
 /* n variables; m_e equality rows (C), m_l rows of A with a finite lower bound,
  * m_u rows of A with a finite upper bound; m_B = m_e + m_l + m_u. */

@@ -29,6 +29,10 @@ EXPORTED = (
     "qpk_apply", "qpk_apply_dev", "qpk_pcg", "qpk_pcg_dev", "qpk_query",
     "qpk_nccl_get_unique_id", "qpk_shard_init", "qpk_ipm_set_bounds", "qpk_ipm_solve",
     "qpk_set_hessian_dense_dev", "qpk_rbf_hessian_dev", "qpk_hessian_apply_dev", "qpk_dense_gemv_dev",
+    "qpk_multi_create", "qpk_multi_destroy", "qpk_multi_devices", "qpk_multi_context", "qpk_multi_problem_begin",
+    "qpk_multi_problem_add_rows", "qpk_multi_set_hessian_diag", "qpk_multi_set_hessian_csr",
+    "qpk_multi_set_hessian_dense", "qpk_multi_set_hessian_lowrank", "qpk_multi_problem_finalize",
+    "qpk_multi_set_diagonals", "qpk_multi_jacobi", "qpk_multi_apply", "qpk_multi_pcg", "qpk_multi_query",
 )
 
 
@@ -105,6 +109,22 @@ _SIGS = {
     "qpk_shard_init": ([_P, _I, _I, _P], _I),
     "qpk_ipm_set_bounds": ([_P, _P, _P, _I64, _P, _P, _I64, _P, _P], _I),
     "qpk_ipm_solve": ([_P, ctypes.POINTER(IpmConfig), _P, _P, ctypes.POINTER(IpmResult)], _I),
+    "qpk_multi_create": ([_I, ctypes.POINTER(_I), ctypes.POINTER(_P)], _I),
+    "qpk_multi_destroy": ([_P], _I),
+    "qpk_multi_devices": ([_P], _I),
+    "qpk_multi_context": ([_P, _I], _P),
+    "qpk_multi_problem_begin": ([_P, _I64, _I64, _I64, _I64], _I),
+    "qpk_multi_problem_add_rows": ([_P, _I64, _P, _P, _P, _P, _I64, _D], _I),
+    "qpk_multi_set_hessian_diag": ([_P, _P], _I),
+    "qpk_multi_set_hessian_csr": ([_P, _P, _P, _P], _I),
+    "qpk_multi_set_hessian_dense": ([_P, _P], _I),
+    "qpk_multi_set_hessian_lowrank": ([_P, _P, _I64, _P, _P], _I),
+    "qpk_multi_problem_finalize": ([_P, _I], _I),
+    "qpk_multi_set_diagonals": ([_P, _P, _P], _I),
+    "qpk_multi_jacobi": ([_P, _P], _I),
+    "qpk_multi_apply": ([_P, _P, _P], _I),
+    "qpk_multi_pcg": ([_P, _P, _D, _I, _I64, _P, ctypes.POINTER(PcgInfo), _P], _I),
+    "qpk_multi_query": ([_P, _I, ctypes.c_char_p], _I64),
 }
 
 _lib = None
@@ -165,3 +185,35 @@ class Context:
 
     def query(self, key: str) -> int:
         return int(self._lib.qpk_query(self._h, key.encode()))
+
+
+class MultiContext:
+    """One libqpk multi-device object (qpk_multi): several GPUs, one process."""
+
+    def __init__(self, devices):
+        lib = load_library()
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
+        h = ctypes.c_void_p()
+        rc = lib.qpk_multi_create(len(devices), devs, ctypes.byref(h))
+        if rc != QPK_OK:
+            raise NativeUnavailable(lib.qpk_last_error().decode(errors="replace"))
+        self._lib = lib
+        self._h = h
+        self.devices = list(devices)
+
+    def close(self):
+        if self._h:
+            self._lib.qpk_multi_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def call(self, name, *args):
+        check(name, getattr(self._lib, name)(self._h, *args))
+
+    def query(self, key: str, rank: int = 0) -> int:
+        return int(self._lib.qpk_multi_query(self._h, int(rank), key.encode()))

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 #include <dlfcn.h>
 
@@ -536,6 +537,9 @@ struct qpk_ctx {
   bool cacc = false;
   int tile_grid = 0;
   bool h_symmetric = true;
+  DBuf<int> hown;                 // sharded, CSR H: the H rows this rank applies (RCM order)
+  std::vector<int> h_own;
+  bool h_own_set = false;
   DBuf<int> tile_beg, cta_off, tslot, col_ptr2, col_pos2, comb_beg2, comb_col2;
   DBuf<double> cpart;
   int comb_lanes2 = 8, comb_nseg2 = 0, comb_max2 = 0;   // max CTA partials of one column
@@ -614,8 +618,10 @@ struct qpk_ctx {
     o.H.kind = hkind; o.H.h = hh.p; o.H.rp = hrp.p; o.H.ci = hci.p; o.H.v = hv.p; o.H.lanes = h_lanes;
     o.H.dense = hdense.p; o.H.U = U.p; o.H.w = w.p; o.H.k = (int)hk;
     o.H.sym = hsym.p; o.H.chunks = hchunks.p; o.H.nchunks = h_nchunks;
+    o.H.rows = h_own_set ? hown.p : nullptr; o.H.nrows = h_own_set ? (int)h_own.size() : 0;
     o.d = d.p; o.q = q.p;
     o.top_owner = rank == 0 ? 1 : 0;
+    o.t_lo = (int)(n * rank / world); o.t_hi = (int)(n * (rank + 1) / world);   // this rank's top slice
     o.r0 = 0; o.ndense = 0; o.cdense = nullptr;        // dense-row split: slot engine only (make_engine)
     return o;
   }
@@ -1132,8 +1138,10 @@ static int build_dict(qpk_ctx* c, bool probe) {
   const size_t n_bcols = cols.size();
   const int n_btiles = tid;
   // the sparse Hessian's rows as dense tiles too (top-block rows, no B'z part),
-  // when they are dense enough -- the owner rank only
-  if (c->hkind == QPK_HESS_CSR && c->rank == 0 && !c->h_hci.empty()) {
+  // when they are dense enough.  Sharded: every rank takes a contiguous,
+  // nnz-balanced slice of the tile-row sequence (the decision to tile is taken
+  // on the whole H, so all ranks agree; H is replicated and small next to B)
+  if (c->hkind == QPK_HESS_CSR && !c->h_hci.empty()) {
     const size_t t0 = tiles.size(), c0 = cols.size(), v0 = tval.size();
     // rows in reverse Cuthill-McKee order: a Hessian like D_t'D_t of randomly
     // numbered band columns is banded in that order, so consecutive rows share
@@ -1142,9 +1150,17 @@ static int build_dict(qpk_ctx* c, bool probe) {
     // empty rows (columns that never meet the objective block) need no tile
     hperm.erase(std::remove_if(hperm.begin(), hperm.end(),
                                [&](int j) { return c->h_hrp[j + 1] == c->h_hrp[j]; }), hperm.end());
-    const long long hs = tile_rows(c->h_hrp.data(), c->h_hci.data(), c->h_hv.data(), (long long)hperm.size(), 1,
-                                   hperm.data());
-    if (hs > 0 && (double)c->h_hci.size() / (double)hs >= 0.5) {
+    long long hs = tile_rows(c->h_hrp.data(), c->h_hci.data(), c->h_hv.data(), (long long)hperm.size(), 1,
+                             hperm.data());
+    const bool tile_h = hs > 0 && (double)c->h_hci.size() / (double)hs >= 0.5;
+    if (tile_h && c->h_own_set) {
+      // keep only the rows this rank applies (its slice of the same sequence), re-tiled on their own
+      tiles.resize(t0); cols.resize(c0); tval.resize(v0); tid = n_btiles;
+      hperm = c->h_own;
+      if (!hperm.empty())
+        hs = tile_rows(c->h_hrp.data(), c->h_hci.data(), c->h_hv.data(), (long long)hperm.size(), 1, hperm.data());
+    }
+    if (tile_h) {
       c->h_tiled = true;
       hperm.resize(hperm.size() + 4, 0);               // the tile kernel bulk-copies 16-byte windows
       CUDA_TRY(upload(c->hperm, hperm, c->stream));
@@ -1545,6 +1561,28 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   // (random B, where no blocking creates reuse).  CSC and DICT are
   // deterministic; DICT falls back to CSC when a row is wider than a dictionary.
   if (const char* ev = getenv("QPK_SCATTER")) if (scatter == QPK_SCATTER_AUTO) scatter = atoi(ev);
+  // Sharded, sparse H: H is replicated; rank r applies a contiguous, nnz-balanced
+  // slice of its non-empty rows in reverse Cuthill-McKee order (the order the
+  // Hessian tiles use), whatever apply format each rank ends up with
+  c->h_own_set = false;
+  c->h_own.clear();
+  if (c->world > 1 && c->hkind == QPK_HESS_CSR) {
+    std::vector<int> seq = rcm_order(c->n, c->h_hrp, c->h_hci);
+    seq.erase(std::remove_if(seq.begin(), seq.end(), [&](int j) { return c->h_hrp[j + 1] == c->h_hrp[j]; }), seq.end());
+    std::vector<long long> pre(seq.size() + 1, 0);
+    for (size_t q = 0; q < seq.size(); ++q) pre[q + 1] = pre[q] + (c->h_hrp[seq[q] + 1] - c->h_hrp[seq[q]]);
+    auto cut = [&](int r) {
+      return (size_t)(std::lower_bound(pre.begin(), pre.end(), pre.back() * r / c->world) - pre.begin());
+    };
+    const size_t q_lo = c->rank == 0 ? 0 : cut(c->rank);
+    const size_t q_hi = c->rank == c->world - 1 ? seq.size() : cut(c->rank + 1);
+    c->h_own.assign(seq.begin() + q_lo, seq.begin() + std::max(q_lo, q_hi));
+    c->h_own_set = true;
+    std::vector<int> up = c->h_own;
+    up.resize(up.size() + 4, 0);
+    CUDA_TRY(upload(c->hown, up, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+  }
   c->scatter = QPK_SCATTER_ATOMIC;
   // a dense column panel (large systems in AUTO) comes first
   if (c->m > 0 && (scatter == QPK_SCATTER_PANEL || (scatter == QPK_SCATTER_AUTO && c->N() >= 50000))) {
@@ -2555,3 +2593,5 @@ int64_t qpk_query(qpk_ctx* c, const char* key) {
 }
 
 }  // extern "C"
+
+#include "qpk_multi.cuh"

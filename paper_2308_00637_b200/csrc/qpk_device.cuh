@@ -29,6 +29,7 @@ struct Hess {
   int kind;
   const double* h;                      // DIAG: d ; LOWRANK: h0
   const int* rp; const int* ci; const double* v; int lanes;  // CSR (full symmetric storage)
+  const int* rows; int nrows;           // CSR, sharded: the H rows this rank applies (null: all n rows)
   const double* dense;                  // n x n row-major
   const double* sym;                    // dense H as packed upper 64 x 64 tiles (null: not built)
   const int4* chunks;                   // sym work units {I, J0, J1, tile of (I, J0)}
@@ -43,7 +44,13 @@ struct Op {
   Hess H;
   const double* d;                      // d_diag, m
   const double* q;                      // q_diag_extra, n
-  int top_owner;                        // this rank adds the (replicated) top-block terms once
+  int top_owner;                        // rank 0: applies a dense / low-rank H (one owner; single GPU: 1)
+  // Sharded runs replicate the top block (n) on every rank.  Each rank OWNS
+  // the slice [t_lo, t_hi) of it: it alone adds diag(Q) p, the sparse-H rows
+  // and the dot-product terms of those entries, so every replicated term is
+  // counted exactly once by the all-reduce -- and the work is spread over the
+  // ranks instead of sitting on rank 0.  Single GPU: [0, n).
+  int t_lo, t_hi;
   // slot engine only: the first ndense rows of B are dense (e.g. the SVM dual's
   // y' alpha = 0 row, n entries) and are handled as dense vectors outside the
   // row pass (dot partials in the top kernel, k_slot_dense); r0 = ndense rows
@@ -164,11 +171,15 @@ __device__ __forceinline__ double subwarp_sum(double s) {
   return s;
 }
 
+// entry i of an N-vector is counted by this rank in a dot product: every
+// bottom entry it holds, and the top entries of its slice
+__device__ __forceinline__ bool owns(const Op& op, int i) { return i >= op.n || (i >= op.t_lo && i < op.t_hi); }
+
 // ------------------------------------------------------------ prep(v) ------
 // y_top = Q_diag-part * v (the part of Q u = H u + q_extra*u that is diagonal)
 // for element j, returns its contribution v_j * y_j to v'Kv.
 __device__ __forceinline__ double prep_elem(const Op& op, int j, double vj, double* y) {
-  if (!op.top_owner) { y[j] = 0.0; return 0.0; }     // other ranks: B'z partial only
+  if (j < op.t_lo || j >= op.t_hi) { y[j] = 0.0; return 0.0; }     // not this rank's slice: B'z partial only
   const int kind = op.H.kind;
   double qv = __dmul_rn(__ldg(op.q + j), vj);
   double t;
@@ -234,23 +245,26 @@ struct RowFuse {
 __device__ __forceinline__ double hess_rows(const Op& op, const double* u, double* y, const double* part, int G,
                                             double* red, double* s_lr) {
   double acc = 0.0;
-  if (!op.top_owner) return 0.0;
+  const int kind = op.H.kind;
+  if (kind != HESS_CSR && !op.top_owner) return 0.0;  // dense / low-rank H: one owner rank
   const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarp = (gridDim.x * blockDim.x) >> 5;
-  const int kind = op.H.kind;
   if (kind == HESS_CSR) {
+    // the H rows this rank applies (sharded: its row list; single GPU: all rows)
     const int LH = op.H.lanes;                       // power of two <= 32
     const int lh = threadIdx.x & (LH - 1);
     const int per = 32 / LH, sw = (threadIdx.x & 31) / LH;
-    for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
-      const int j = (int)jb + sw;
+    const int nr = op.H.rows ? op.H.nrows : op.n;
+    for (long long jb = (long long)gwarp * per; jb < nr; jb += (long long)nwarp * per) {
+      const int q = (int)jb + sw;
+      const int j = q < nr ? (op.H.rows ? __ldg(op.H.rows + q) : q) : 0;
       double s = 0.0;
-      if (j < op.n) {
+      if (q < nr) {
         const int b = __ldg(op.H.rp + j), e = __ldg(op.H.rp + j + 1);
         for (int kk = b + lh; kk < e; kk += LH) s = fma(__ldg(op.H.v + kk), u[__ldg(op.H.ci + kk)], s);
       }
       for (int o = LH / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (j < op.n && lh == 0) { atomicAdd(y + j, s); acc += u[j] * s; }
+      if (q < nr && lh == 0) { atomicAdd(y + j, s); acc += u[j] * s; }
     }
   } else if (kind == HESS_DENSE && op.H.sym) {
     return 0.0;                                        // packed symmetric tiles: hess_sym (own launch)

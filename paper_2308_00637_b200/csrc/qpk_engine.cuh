@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_engine_init(Engine E) {
     const double b = __ldg(E.rhs + i);
     E.x[0][i] = 0.0;
     E.r[i] = b;
-    if (E.op.top_owner || i >= E.op.n) acc += b * b;
+    if (owns(E.op, i)) acc += b * b;
   }
   const double t = block_sum(acc, red);
   if (threadIdx.x == 0) E.part[SLOT_AUX * E.G + blockIdx.x] = t;
@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_top(Engine E, int par) {
       if (c.xupd) xd[j] = __dadd_rn(xs[j], __dmul_rn(c.alpha_prev, pold));
       const double rj = E.r[j];
       const double zj = __dmul_rn(__ldg(E.minv + j), rj);
-      if (op.top_owner) rz += rj * zj;
+      if (j >= op.t_lo && j < op.t_hi) rz += rj * zj;
       const double pn = restart ? zj : __dadd_rn(zj, __dmul_rn(c.beta, pold));
       E.p[j] = pn;
       if (E.panel.cpos) { const int pp = __ldg(E.panel.cpos + j); if (pp >= 0) E.panel.ue[pp] = pn; }
@@ -554,7 +554,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
       const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
       E.r[i] = ri;
-      if (op.top_owner || i >= op.n) {
+      if (owns(op, i)) {
         rr += ri * ri;
         rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
       }
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
             ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yv[u].y));
             r2[i] = ri;
             // replicated top entries count once over the ranks (rank 0)
-            const bool cx = op.top_owner || 2 * i >= op.n, cy = op.top_owner || 2 * i + 1 >= op.n;
+            const bool cx = owns(op, 2 * i), cy = owns(op, 2 * i + 1);
             if (cx) { rr += ri.x * ri.x; rzn += ri.x * __dmul_rn(mv[u].x, ri.x); }
             if (cy) { rr += ri.y * ri.y; rzn += ri.y * __dmul_rn(mv[u].y, ri.y); }
           }
@@ -594,7 +594,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       if ((N & 1) && N - 1 >= nb && blockIdx.x == 0 && threadIdx.x == 0) {
         const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
         E.r[N - 1] = ri;
-        if (op.top_owner || N - 1 >= op.n) {
+        if (owns(op, N - 1)) {
           rr += ri * ri;
           rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
         }
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       const double yi = (CSC && i < op.n) ? top_value<SC>(E, i) : E.y[i];
       const double ri = __dsub_rn(__ldg(E.rhs + i), yi);
       if (store) E.r[i] = ri;
-      if (op.top_owner || i >= op.n) rr += ri * ri;
+      if (owns(op, i)) rr += ri * ri;
     }
   }
   double t = block_sum(rr, red);

@@ -464,14 +464,17 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
   const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
   const Op& op = E.op;
   double acc = 0.0;
-  if (op.H.kind == HESS_CSR && op.top_owner) {
+  if (op.H.kind == HESS_CSR) {
+    // the H rows this rank applies (sharded: its row list; single GPU: all rows)
     const int LH = op.H.lanes, lh = threadIdx.x & (LH - 1);
     const int per = 32 / LH, sw = (threadIdx.x & 31) / LH;
     const int gwarp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarp = (gridDim.x * blockDim.x) >> 5;
-    for (long long jb = (long long)gwarp * per; jb < op.n; jb += (long long)nwarp * per) {
-      const int j = (int)jb + sw;
+    const int nr = op.H.rows ? op.H.nrows : op.n;
+    for (long long jb = (long long)gwarp * per; jb < nr; jb += (long long)nwarp * per) {
+      const int q = (int)jb + sw;
+      const int j = q < nr ? (op.H.rows ? __ldg(op.H.rows + q) : q) : 0;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      if (j < op.n) {
+      if (q < nr) {
         const int b = __ldg(op.H.rp + j), e = __ldg(op.H.rp + j + 1);
         int k = b + lh;
         for (; k + 3 * LH < e; k += 4 * LH) {
@@ -486,7 +489,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
       }
       double sum = (s0 + s1) + (s2 + s3);
       for (int o = LH / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-      if (j < op.n && lh == 0) { E.y[j] += sum; acc += v[j] * sum; }
+      if (q < nr && lh == 0) { E.y[j] += sum; acc += v[j] * sum; }
     }
   } else if (op.H.kind == HESS_DENSE && op.H.sym) {
     acc = hess_sym(op, v, E.y);                     // packed symmetric tiles (large dense H)

@@ -128,6 +128,102 @@ class GpuKkt:
         self.ctx.close()
 
 
+class MultiGpuKkt(GpuKkt):
+    """The same operator row-sharded over several GPUs, driven from THIS process
+    (qpk_multi, include/qpk.h): the reference's single-process solve()
+    (ipm.py:185-206) can use N GPUs through the unmodified hook.  Same methods
+    and global-sized vectors as GpuKkt."""
+
+    def __init__(self, problem, bmap, devices, scatter: int = _native.QPK_SCATTER_AUTO):
+        self.ctx = _native.MultiContext(devices)
+        self.devices = list(devices)
+        self.n = int(problem.n)
+        lin_lower = np.ascontiguousarray(bmap.lin_lower, dtype=np.int64)
+        lin_upper = np.ascontiguousarray(bmap.lin_upper, dtype=np.int64)
+        m_e = int(problem.c.n_rows)
+        self.m = m_e + len(lin_lower) + len(lin_upper)
+        self.dim = self.n + self.m
+        c = self.ctx
+        keep = []                                    # the library reads these arrays at finalize
+        c.call("qpk_multi_problem_begin", self.n, m_e, len(lin_lower), len(lin_upper))
+        if m_e:
+            ro, ci, v = _csr_arrays(problem.c)
+            keep += [ro, ci, v]
+            c.call("qpk_multi_problem_add_rows", int(problem.c.n_rows), _native.ptr(ro), _native.ptr(ci),
+                   _native.ptr(v), None, 0, 1.0)
+        if len(lin_lower) or len(lin_upper):
+            ro, ci, v = _csr_arrays(problem.a)
+            keep += [ro, ci, v]
+            for rows, sign in ((lin_lower, 1.0), (lin_upper, -1.0)):
+                if len(rows):
+                    c.call("qpk_multi_problem_add_rows", int(problem.a.n_rows), _native.ptr(ro), _native.ptr(ci),
+                           _native.ptr(v), _native.ptr(rows), len(rows), sign)
+        keep += self._set_hessian_multi(problem.hessian)
+        c.call("qpk_multi_problem_finalize", int(scatter))
+        del keep
+        self._hist = None
+
+    def _set_hessian_multi(self, h):
+        kind = type(h).__name__
+        c = self.ctx
+        if kind == "DiagonalHessian":
+            d = np.ascontiguousarray(h.d, dtype=np.float64)
+            _dim(len(d), self.n, "Hessian")
+            c.call("qpk_multi_set_hessian_diag", _native.ptr(d))
+            return [d]
+        if kind == "SparseHessian":
+            ro, ci, v = _csr_arrays(h.m)
+            _dim(h.m.n_rows, self.n, "Hessian")
+            c.call("qpk_multi_set_hessian_csr", _native.ptr(ro), _native.ptr(ci), _native.ptr(v))
+            return [ro, ci, v]
+        if kind == "DenseHessian":
+            mm = np.ascontiguousarray(h.m, dtype=np.float64)
+            if mm.ndim != 2 or mm.shape != (self.n, self.n):
+                from .problem import DimensionError
+                raise DimensionError(f"dense Hessian has shape {mm.shape}, expected {(self.n, self.n)}")
+            c.call("qpk_multi_set_hessian_dense", _native.ptr(mm))
+            return [mm]
+        if kind == "QuasiNewtonHessian":
+            h0 = np.ascontiguousarray(h.h0_diag, dtype=np.float64)
+            u = np.ascontiguousarray(h.u, dtype=np.float64)
+            w = np.ascontiguousarray(h.w, dtype=np.float64)
+            _dim(len(h0), self.n, "Hessian")
+            c.call("qpk_multi_set_hessian_lowrank", _native.ptr(h0), int(u.shape[1]), _native.ptr(u), _native.ptr(w))
+            return [h0, u, w]
+        raise TypeError(f"unsupported Hessian type {kind}")
+
+    def set_diagonals(self, d_diag, q_extra):
+        d = np.ascontiguousarray(d_diag, dtype=np.float64)
+        q = np.ascontiguousarray(q_extra, dtype=np.float64)
+        _dim(len(d), self.m, "d_diag")
+        _dim(len(q), self.n, "q_diag_extra")
+        self.ctx.call("qpk_multi_set_diagonals", _native.ptr(d), _native.ptr(q))
+
+    def jacobi(self) -> np.ndarray:
+        out = np.empty(self.dim)
+        self.ctx.call("qpk_multi_jacobi", _native.ptr(out))
+        return out
+
+    def apply(self, v) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        _dim(len(v), self.dim, "vector")
+        y = np.empty(self.dim)
+        self.ctx.call("qpk_multi_apply", _native.ptr(v), _native.ptr(y))
+        return y
+
+    def pcg(self, rhs, tol: float, max_iters: int, tol_is_relative: bool = True, history: bool = False):
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        _dim(len(rhs), self.dim, "rhs")
+        x = np.empty(self.dim)
+        info = _native.PcgInfo()
+        hist = np.full(int(max_iters) + 1, np.nan) if history else None
+        self.ctx.call("qpk_multi_pcg", _native.ptr(rhs), float(tol), int(bool(tol_is_relative)), int(max_iters),
+                      _native.ptr(x), _native.ctypes.byref(info), _native.ptr(hist) if history else None)
+        if history:
+            hist = hist[: info.iterations + 1]
+        return x, info, hist
+
+
 def _dim(got, want, what):
     if got != want:
         from .problem import DimensionError
@@ -151,6 +247,29 @@ def _finalizer(key):
         entry[1].close()
 
 
+_DEVICES = None
+
+
+def set_devices(devices):
+    """GPUs the drop-in hook uses: None / one id = a single GPU (GpuKkt); a list
+    of several ids = one process driving them all (MultiGpuKkt).  The hook's
+    signature is the reference's, so the choice is made here (or through the
+    environment: QPK_DEVICES=0,1,2,3)."""
+    global _DEVICES
+    _DEVICES = None if devices is None else [int(d) for d in np.atleast_1d(devices)]
+    for key in list(_CACHE):
+        _finalizer(key)
+
+
+def _devices(default: int):
+    if _DEVICES is not None:
+        return _DEVICES
+    env = os.environ.get("QPK_DEVICES")
+    if env:
+        return [int(t) for t in env.split(",") if t.strip() != ""]
+    return [default]
+
+
 def operator_for(op, device: int = 0) -> GpuKkt:
     problem = op.problem
     key = id(problem)
@@ -163,7 +282,10 @@ def operator_for(op, device: int = 0) -> GpuKkt:
             return entry[1]
     if entry is not None:
         _finalizer(key)
-    gk = GpuKkt(problem, op.bmap, device=device)
+    devs = _devices(device)
+    # (QPK_MULTI=1 sends even a single device through the multi-device layer: its one-GPU test)
+    single = len(devs) == 1 and not os.environ.get("QPK_MULTI")
+    gk = GpuKkt(problem, op.bmap, device=devs[0]) if single else MultiGpuKkt(problem, op.bmap, devs)
     try:
         ref = weakref.ref(problem, lambda _r, k=key: _finalizer(k))
     except TypeError:

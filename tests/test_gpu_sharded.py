@@ -62,3 +62,62 @@ def test_sharded_world1_parity(group, name, mode):
         assert info.converged
         assert parity.rel_err(x, CFG[pre + "pcg_x"]) <= 1e-5
     sk.close()
+
+
+# ------------------------------------------------ one process, several GPUs --
+@pytest.mark.parametrize("mode", [_native.QPK_SCATTER_AUTO, _native.QPK_SCATTER_CSC, _native.QPK_SCATTER_DICT])
+@pytest.mark.parametrize("name", sorted(SPECS))
+def test_multi_device_context_world1(name, mode):
+    """qpk_multi (one process driving a device list; include/qpk.h) with a
+    one-device list: the row-sharding layer, the NCCL communicator created
+    from the device threads and every collective of the sharded slot run on
+    the one GPU this box has.  Global vectors in and out, no torch.distributed."""
+    from paper_2308_00637_b200.direction import MultiGpuKkt
+    fn, kw = SPECS[name]
+    problem, state, meta = fn(**kw)
+    op = build_operator(problem, state)
+    pre = name + "_"
+    mk = MultiGpuKkt(problem, op.bmap, devices=[0], scatter=mode)
+    assert mk.ctx.query("world") == 1 and mk.ctx.query("engine") == 1
+    assert mk.ctx.query("row_lo") == 0 and mk.ctx.query("row_hi") == op.m
+    mk.set_diagonals(op.d_diag, op.q_diag_extra)
+    assert parity.rel_err(mk.jacobi(), CFG[pre + "jacobi"]) <= parity.APPLY_TOL
+    for v, y in zip(CFG[pre + "vecs"], CFG[pre + "applies"]):
+        assert parity.rel_err(mk.apply(v), y) <= parity.APPLY_TOL
+    rhs = CFG[pre + "rhs"]
+    cfg = orc.PcgConfig(tol=1e-300, max_iters=200) if name == "cfg5" else orc.PcgConfig(tol=1e-7, max_iters=400)
+    x, info, hist = mk.pcg(rhs, cfg.tol, cfg.max_iters, True, history=True)
+    ok, msg = parity.check_history(hist, CFG[pre + "pcg_hist"], parity.envelope(op, rhs, cfg, CFG[pre + "pcg_hist"]))
+    assert ok, msg
+    if int(CFG[pre + "pcg_conv"]):
+        assert info.converged and parity.rel_err(x, CFG[pre + "pcg_x"]) <= 1e-5
+    # a second problem on the same object (communicator reused, shard rebuilt)
+    mk.close()
+
+
+def test_hook_through_multi_device_layer(monkeypatch):
+    """gpu_direction(op, rhs, cfg) with QPK_DEVICES / QPK_MULTI selecting the
+    multi-device layer: same PcgResult as the single-GPU operator."""
+    from paper_2308_00637_b200 import direction
+    from paper_2308_00637_b200.pcg import PcgConfig
+    problem, state, meta = workloads.rt_like(seed=3, n_vox=6000, n_beam=600, density=0.02)
+    op = build_operator(problem, state)
+    rhs = CFG["cfg3_rhs"]
+    cfg = PcgConfig(tol=1e-7, max_iters=400)
+    direction.set_devices(None)
+    single = direction.gpu_direction(op, rhs, cfg)
+    monkeypatch.setenv("QPK_MULTI", "1")
+    direction.set_devices([0])
+    try:
+        multi = direction.gpu_direction(op, rhs, cfg)
+        assert isinstance(direction.operator_for(op), direction.MultiGpuKkt)
+    finally:
+        direction.set_devices(None)
+    assert multi.converged == single.converged
+    assert parity.rel_err(multi.solution, single.solution) <= 1e-6
+    assert parity.rel_err(multi.solution, CFG["cfg3_pcg_x"]) <= 1e-5
+
+
+def test_multi_device_rejects_duplicate_devices():
+    with pytest.raises(_native.NativeUnavailable, match="listed twice"):
+        _native.MultiContext([0, 0])

@@ -1,8 +1,8 @@
 """Multi-GPU path on CPU: world_size 2, gloo.
 
 The device kernels cannot run here, so each rank executes the SAME sharded
-algorithm the library runs per slot (qpk_engine.cuh: top-owner counting of
-the replicated top block, rank-local B rows, one all-reduce of
+algorithm the library runs per slot (qpk_engine.cuh: every rank owns a slice
+of the replicated top block and of the Hessian rows, rank-local B rows, one all-reduce of
 [y_top partial | scalars] and one of [r'r, r'z]) with numpy on its shard, the
 collectives going through torch.distributed/gloo.  The result must equal the
 oracle's single-process operator apply and PCG (bit-for-bit is not expected:
@@ -52,7 +52,23 @@ class ShardEmulation:
         self.d_loc = op.d_diag[self.lo:self.hi]
         self.q = op.q_diag_extra
         self.h = p.hessian
-        self.owner = rank == 0
+        # the replicated top block is split into owned slices: rank r alone adds
+        # diag(Q) u and the dot-product terms of [t_lo, t_hi), and applies a
+        # contiguous, nnz-balanced slice of the sparse Hessian's non-empty rows
+        # (the library slices them in RCM order; any fixed sequence partitions H)
+        self.t_lo, self.t_hi = p.n * rank // world, p.n * (rank + 1) // world
+        self.hrows = None
+        if type(self.h).__name__ == "SparseHessian":
+            hm = orc._csr(self.h.m)
+            lens = np.diff(hm.indptr)
+            seq = np.nonzero(lens)[0]
+            pre = np.concatenate([[0], np.cumsum(lens[seq])])
+            cut = lambda r: int(np.searchsorted(pre, pre[-1] * r // world, side="left"))  # noqa: E731
+            lo = 0 if rank == 0 else cut(rank)
+            hi = len(seq) if rank == world - 1 else cut(rank + 1)
+            self.hrows = seq[lo:max(lo, hi)]
+            self.hm = hm
+        self.h_owner = rank == 0                      # dense / low-rank H: one owner
 
     def apply(self, v_loc):
         """K v restricted to this rank: y_top (global after the all-reduce), local y_bottom."""
@@ -60,14 +76,21 @@ class ShardEmulation:
         t = self.b_loc @ u
         z = 2.0 * t / self.d_loc + w
         top = self.b_loc.T @ z
-        if self.owner:
-            top = top + (orc.hessian_apply(self.h, u) + self.q * u)
+        sl = slice(self.t_lo, self.t_hi)
+        top[sl] += self.q[sl] * u[sl]
+        kind = type(self.h).__name__
+        if kind == "DiagonalHessian":
+            top[sl] += self.h.d[sl] * u[sl]
+        elif kind == "SparseHessian":
+            top[self.hrows] += self.hm[self.hrows] @ u
+        elif self.h_owner:
+            top = top + orc.hessian_apply(self.h, u)
         top = _allreduce(top)
         return np.concatenate([top, t + self.d_loc * w])
 
     def dot(self, a, b):
         """Global dot of two local vectors: the replicated top counted once."""
-        own = float(a[:self.n] @ b[:self.n]) if self.owner else 0.0
+        own = float(a[self.t_lo:self.t_hi] @ b[self.t_lo:self.t_hi])
         return float(_allreduce(np.array([own + float(a[self.n:] @ b[self.n:])]))[0])
 
     def jacobi(self):
