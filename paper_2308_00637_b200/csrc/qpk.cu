@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -495,6 +496,25 @@ NcclApi& nccl() {
   return api;
 }
 
+// Host threads for the format builders (the box has far more cores than the
+// one a serial build uses; the result does not depend on the thread count)
+static int host_threads() {
+  if (const char* ev = getenv("QPK_HOST_THREADS")) return std::max(1, std::min(64, atoi(ev)));
+  const unsigned hc = std::thread::hardware_concurrency();
+  return (int)std::max(1u, std::min(16u, hc ? hc : 4u));
+}
+
+template <typename F>
+static void parallel_chunks(int nchunks, F fn) {
+  const int T = std::min(host_threads(), nchunks);
+  if (T <= 1) { for (int k = 0; k < nchunks; ++k) fn(k); return; }
+  std::atomic<int> next(0);
+  std::vector<std::thread> th;
+  for (int t = 0; t < T; ++t)
+    th.emplace_back([&] { for (int k = next++; k < nchunks; k = next++) fn(k); });
+  for (auto& t : th) t.join();
+}
+
 constexpr int NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
 }  // namespace
@@ -544,9 +564,6 @@ struct qpk_ctx {
   DBuf<double> cpart;
   int comb_lanes2 = 8, comb_nseg2 = 0, comb_max2 = 0;   // max CTA partials of one column
   DBuf<double> tval;
-  DBuf<int4> rtile_desc;
-  int n_rtiles = 0;
-  int tma_rows = -1;              // -1 auto (env QPK_TMA_ROWS)
   DBuf<double> bpart;
   int nblk = 0;
   bool have_dict = false, h_tiled = false;
@@ -857,34 +874,43 @@ int qpk_problem_add_rows(qpk_ctx* c, int64_t n_rows, const int64_t* ro, const in
   const int64_t count = rows ? n_sel : n_rows;
   const long long mB = c->m_e + c->m_l + c->m_u;
   if (c->m + count > mB) return fail(QPK_E_ARG, "qpk_problem_add_rows: more rows than m_B=%lld", mB);
-  {
-    // one reservation for the whole call (rows padded to 4 entries)
-    size_t add = 0;
-    for (int64_t s = 0; s < count; ++s) {
-      const int64_t i = rows ? rows[s] : s;
-      if (i >= 0 && i < n_rows && ro[i + 1] >= ro[i]) add += (size_t)((ro[i + 1] - ro[i] + 3) & ~3LL);
-    }
-    c->h_ci.reserve(c->h_ci.size() + add);
-    c->h_v.reserve(c->h_v.size() + add);
-    c->h_rp.reserve(c->h_rp.size() + (size_t)count);
-  }
+  // validate the selection and lay the rows out (padded to 4 entries), then
+  // convert them on the host threads
+  std::vector<size_t> at((size_t)count + 1, c->h_ci.size());
   for (int64_t s = 0; s < count; ++s) {
     const int64_t i = rows ? rows[s] : s;
     if (i < 0 || i >= n_rows) return fail(QPK_E_ARG, "qpk_problem_add_rows: row index %lld out of range", (long long)i);
-    const int64_t b = ro[i], e = ro[i + 1];
-    if (e < b) return fail(QPK_E_ARG, "row_offsets must be nondecreasing");
-    for (int64_t k = b; k < e; ++k) {
-      const int64_t col = ci[k];
-      if (col < 0 || col >= c->n) return fail(QPK_E_ARG, "column index %lld out of range", (long long)col);
-      c->h_ci.push_back((int)col);
-      c->h_v.push_back(sign * vals[k]);
-    }
-    c->nnz += e - b;
-    while (c->h_ci.size() & 3) { c->h_ci.push_back(-1); c->h_v.push_back(0.0); }
-    if (c->h_ci.size() >= (size_t)(1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "nnz exceeds int32 range");
-    c->h_rp.push_back((int)c->h_ci.size());
-    c->m += 1;
+    if (ro[i + 1] < ro[i]) return fail(QPK_E_ARG, "row_offsets must be nondecreasing");
+    at[s + 1] = at[s] + (size_t)((ro[i + 1] - ro[i] + 3) & ~3LL);
+    c->nnz += ro[i + 1] - ro[i];
   }
+  if (at[count] >= (size_t)(1LL << 31) - 64) return fail(QPK_E_UNSUPPORTED, "nnz exceeds int32 range");
+  c->h_ci.resize(at[count], -1);
+  c->h_v.resize(at[count], 0.0);
+  const size_t rp0 = c->h_rp.size();
+  c->h_rp.resize(rp0 + (size_t)count);
+  const int nchunks = (int)std::max<int64_t>(1, std::min<int64_t>(256, count / 4096));
+  std::atomic<long long> bad_col(-1);
+  int* hci = c->h_ci.data();
+  double* hv = c->h_v.data();
+  int* hrp = c->h_rp.data() + rp0;
+  const int64_t ncols = c->n;
+  parallel_chunks(nchunks, [&](int k) {
+    const int64_t s0 = count * k / nchunks, s1 = count * (k + 1) / nchunks;
+    for (int64_t s = s0; s < s1; ++s) {
+      const int64_t i = rows ? rows[s] : s;
+      size_t o = at[s];
+      for (int64_t e = ro[i]; e < ro[i + 1]; ++e, ++o) {
+        const int64_t col = ci[e];
+        if (col < 0 || col >= ncols) { bad_col = col; return; }
+        hci[o] = (int)col;
+        hv[o] = sign * vals[e];
+      }
+      hrp[s] = (int)at[s + 1];
+    }
+  });
+  if (bad_col.load() != -1) return fail(QPK_E_ARG, "column index %lld out of range", bad_col.load());
+  c->m += count;
   return QPK_OK;
 }
 
@@ -1064,77 +1090,158 @@ static std::vector<int> rcm_order(long long n, const std::vector<int>& rp, const
   return order;
 }
 
-// Dense row tiles: consecutive rows grouped while (rows x padded distinct
-// columns) fits QPK_TILE_DOUBLES, each tile stored as a dense block over its
-// sorted column list.  have_dict = false when a single row is too wide.
-// probe = true (AUTO selection): give up after the first 64k rows when the
-// tiles come out sparse (random B: a tile is ~3 % nonzeros, and the full
-// dense-tile copy would be ~16 GB on cfg5 only to be rejected)
+struct TileOut {
+  std::vector<TileDescD> tiles;
+  std::vector<int> cols;
+  std::vector<double> tval;
+  long long slots = 0;
+  bool too_wide = false;        // a single row does not fit a tile
+};
+
+// Tile the rows [q0, q1) of a CSR matrix (tile row q is matrix row perm[q], or
+// q): consecutive rows grouped while (rows x padded distinct columns) fits
+// QPK_TILE_DOUBLES, each tile a dense block over its sorted column list.
+// d0 / v0 of the descriptors are offsets into o.cols / o.tval.
+static void tile_range(const int* rp, const int* ci, const double* v, const int* perm, long long q0, long long q1,
+                       int kind, std::vector<int>& mark, int& stamp, TileOut& o) {
+  auto r4 = [](long long x) { return (x + 3) & ~3LL; };
+  auto R = [&](long long q) -> long long { return perm ? perm[q] : q; };
+  std::vector<int> cur;
+  cur.reserve(QPK_TILE_DMAX);
+  long long r = q0;
+  while (r < q1) {
+    const long long ra = r;
+    cur.clear();
+    ++stamp;
+    while (r < q1) {
+      long long fresh = 0;
+      for (int k = rp[R(r)]; k < rp[R(r) + 1]; ++k)
+        if (ci[k] >= 0 && mark[ci[k]] != stamp) ++fresh;
+      const long long nd = (long long)cur.size() + fresh, rows = r - ra + 1;
+      if (r4(nd) > QPK_TILE_DMAX || rows * (r4(nd) | 1) > QPK_TILE_DOUBLES || rows > QPK_TILE_ROWS) {
+        if (r == ra) { o.too_wide = true; return; }
+        break;
+      }
+      for (int k = rp[R(r)]; k < rp[R(r) + 1]; ++k)
+        if (ci[k] >= 0 && mark[ci[k]] != stamp) { mark[ci[k]] = stamp; cur.push_back(ci[k]); }
+      ++r;
+    }
+    std::sort(cur.begin(), cur.end());
+    const int ndp = (int)r4((long long)cur.size());
+    const int pitch = ndp | 1;                        // odd row pitch: conflict-free column reads
+    TileDescD td;
+    td.ra = (int)ra; td.rb = (int)r; td.d0 = (int)o.cols.size(); td.ndp = ndp;
+    td.v0 = (int)((o.tval.size() + 1) & ~(size_t)1);  // 16-byte aligned block start
+    td.pad0 = pitch; td.pad1 = kind; td.pad2 = 0;
+    if ((long long)td.v0 + (r - ra) * pitch >= (1LL << 31) - 64) { o.too_wide = true; return; }
+    for (int col : cur) o.cols.push_back(col);
+    for (int i = (int)cur.size(); i < ndp; ++i) o.cols.push_back(-1);
+    const size_t base = td.v0;
+    o.tval.resize(base + (size_t)(r - ra) * pitch, 0.0);
+    for (long long rr = ra; rr < r; ++rr)
+      for (int k = rp[R(rr)]; k < rp[R(rr) + 1]; ++k) {
+        if (ci[k] < 0) continue;
+        const int pos = (int)(std::lower_bound(cur.begin(), cur.end(), ci[k]) - cur.begin());
+        o.tval[base + (size_t)(rr - ra) * pitch + pos] = v[k];
+      }
+    o.slots += (r - ra) * pitch;
+    o.tiles.push_back(td);
+  }
+}
+
+// The rows [0, nrows) tiled in nnz-balanced chunks on the host threads (tiles
+// end at chunk boundaries; the chunking depends on the matrix only), appended
+// to tiles / cols / tval.  Returns the dense slots, or -1 (a row too wide, or
+// the tile storage would exceed the int32 offsets).
+static long long tile_rows_parallel(const int* rp, const int* ci, const double* v, const int* perm, long long nrows,
+                                    int kind, long long n, std::vector<TileDescD>& tiles, std::vector<int>& cols,
+                                    std::vector<double>& tval) {
+  if (nrows <= 0) return 0;
+  int C = perm ? 1 : (int)std::max<long long>(1, std::min<long long>(512, nrows / 2048));
+  std::vector<long long> cut(C + 1, 0);
+  cut[C] = nrows;
+  for (int k = 1; k < C; ++k) {
+    const long long want = (long long)rp[0] + ((long long)rp[nrows] - rp[0]) * k / C;
+    cut[k] = std::max(cut[k - 1], (long long)(std::lower_bound(rp, rp + nrows, (int)want) - rp));
+  }
+  std::vector<TileOut> outs(C);
+  {
+    const int T = std::min(host_threads(), C);
+    std::vector<std::vector<int>> marks(T);
+    std::atomic<int> next(0), slot(0);
+    auto work = [&] {
+      const int me = slot++;
+      marks[me].assign(n, 0);
+      int stamp = 0;
+      for (int k = next++; k < C; k = next++)
+        tile_range(rp, ci, v, perm, cut[k], cut[k + 1], kind, marks[me], stamp, outs[k]);
+    };
+    if (T <= 1) {
+      work();
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(work);
+      for (auto& t : th) t.join();
+    }
+  }
+  long long slots = 0;
+  std::vector<size_t> cb(C + 1, cols.size()), vb(C + 1, (tval.size() + 1) & ~(size_t)1), tb(C + 1, tiles.size());
+  for (int k = 0; k < C; ++k) {
+    if (outs[k].too_wide) return -1;
+    slots += outs[k].slots;
+    cb[k + 1] = cb[k] + outs[k].cols.size();
+    vb[k + 1] = vb[k] + ((outs[k].tval.size() + 1) & ~(size_t)1);
+    tb[k + 1] = tb[k] + outs[k].tiles.size();
+  }
+  if (vb[C] >= (size_t)(1LL << 31) - 64 || cb[C] >= (size_t)(1LL << 31) - 64) return -1;
+  cols.resize(cb[C]);
+  tval.resize(vb[C], 0.0);
+  tiles.resize(tb[C]);
+  parallel_chunks(C, [&](int k) {
+    TileOut& o = outs[k];
+    if (!o.cols.empty()) memcpy(cols.data() + cb[k], o.cols.data(), o.cols.size() * sizeof(int));
+    if (!o.tval.empty()) memcpy(tval.data() + vb[k], o.tval.data(), o.tval.size() * sizeof(double));
+    for (size_t t = 0; t < o.tiles.size(); ++t) {
+      TileDescD td = o.tiles[t];
+      td.d0 += (int)cb[k];
+      td.v0 += (int)vb[k];
+      tiles[tb[k] + t] = td;
+    }
+    std::vector<double>().swap(o.tval);
+    std::vector<int>().swap(o.cols);
+  });
+  return slots;
+}
+
+// Dense row tiles for clustered B (and a sparse Hessian).  have_dict = false
+// when a single row is too wide.  probe = true (AUTO selection): give up when
+// the first 64k rows tile sparsely (random B: a tile is ~3 % nonzeros, and the
+// full dense-tile copy would be ~16 GB on cfg5 only to be rejected)
 static int build_dict(qpk_ctx* c, bool probe) {
   c->have_dict = false;
   c->h_tiled = false;
   const long long n = c->n, m = c->m;
-  std::vector<int> mark(n, -1), cur;
   std::vector<TileDescD> tiles;
   std::vector<int> cols;
   std::vector<double> tval;
-  cur.reserve(QPK_TILE_DMAX);
-  int tid = 0;
-  auto r4 = [](long long x) { return (x + 3) & ~3LL; };
-  // tile the rows [0, nrows) of a CSR matrix; returns dense slots, or -1 if a
-  // row is wider than a tile
+  if (probe && m > 65536) {
+    TileOut o;
+    std::vector<int> mark(n, 0);
+    int stamp = 0;
+    tile_range(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), nullptr, 0, 65536, 0, mark, stamp, o);
+    if (o.too_wide) return QPK_OK;
+    if ((double)c->h_rp[65536] < 0.3 * (double)o.slots) {
+      c->dict_reuse = (double)c->h_rp[65536] / (double)o.slots;       // estimate from the probed rows
+      return QPK_OK;
+    }
+  }
   auto tile_rows = [&](const int* rp, const int* ci, const double* v, long long nrows, int kind,
                        const int* perm) -> long long {
-    long long slots = 0, r = 0;
-    auto R = [&](long long q) -> long long { return perm ? perm[q] : q; };
-    while (r < nrows) {
-      const long long ra = r;
-      cur.clear();
-      while (r < nrows) {
-        long long fresh = 0;
-        for (int k = rp[R(r)]; k < rp[R(r) + 1]; ++k)
-          if (ci[k] >= 0 && mark[ci[k]] != tid) ++fresh;
-        const long long nd = (long long)cur.size() + fresh, rows = r - ra + 1;
-        if (r4(nd) > QPK_TILE_DMAX || rows * (r4(nd) | 1) > QPK_TILE_DOUBLES || rows > QPK_TILE_ROWS) {
-          if (r == ra) return -1;
-          break;
-        }
-        for (int k = rp[R(r)]; k < rp[R(r) + 1]; ++k)
-          if (ci[k] >= 0 && mark[ci[k]] != tid) { mark[ci[k]] = tid; cur.push_back(ci[k]); }
-        ++r;
-      }
-      std::sort(cur.begin(), cur.end());
-      const int ndp = (int)r4((long long)cur.size());
-      const int pitch = ndp | 1;                        // odd row pitch: conflict-free column reads
-      TileDescD td;
-      td.ra = (int)ra; td.rb = (int)r; td.d0 = (int)cols.size(); td.ndp = ndp;
-      td.v0 = (int)((tval.size() + 1) & ~(size_t)1);  // 16-byte aligned block start
-      td.pad0 = pitch; td.pad1 = kind; td.pad2 = 0;
-      if ((long long)td.v0 + (r - ra) * pitch >= (1LL << 31) - 64) return -1;
-      for (int col : cur) cols.push_back(col);
-      for (int i = (int)cur.size(); i < ndp; ++i) cols.push_back(-1);
-      const size_t base = td.v0;
-      tval.resize(base + (size_t)(r - ra) * pitch, 0.0);
-      for (long long rr = ra; rr < r; ++rr)
-        for (int k = rp[R(rr)]; k < rp[R(rr) + 1]; ++k) {
-          if (ci[k] < 0) continue;
-          const int pos = (int)(std::lower_bound(cur.begin(), cur.end(), ci[k]) - cur.begin());
-          tval[base + (size_t)(rr - ra) * pitch + pos] = v[k];
-        }
-      slots += (r - ra) * pitch;
-      tiles.push_back(td);
-      ++tid;
-      if (probe && kind == 0 && !perm && ra < 65536 && r >= 65536 && r < nrows &&
-          (double)rp[r] < 0.3 * (double)slots) {
-        c->dict_reuse = (double)rp[r] / (double)slots;      // estimate from the probed rows
-        return -2;
-      }
-    }
-    return slots;
+    return tile_rows_parallel(rp, ci, v, perm, nrows, kind, n, tiles, cols, tval);
   };
-  tval.reserve(c->h_ci.size() + c->h_ci.size() / 4 + 64);
   const long long slots = tile_rows(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), m, 0, nullptr);
-  if (slots < 0) return QPK_OK;                       // a row wider than a tile, or sparse tiles (probe)
+  if (slots < 0) return QPK_OK;                       // a row wider than a tile
+  int tid = (int)tiles.size();
   const size_t n_bcols = cols.size();
   const int n_btiles = tid;
   // the sparse Hessian's rows as dense tiles too (top-block rows, no B'z part),
@@ -1168,6 +1275,7 @@ static int build_dict(qpk_ctx* c, bool probe) {
       tiles.resize(t0); cols.resize(c0); tval.resize(v0); tid = n_btiles;
     }
   }
+  tid = (int)tiles.size();
   // column -> its B-tile-partial positions, in tile order
   std::vector<int> col_ptr(n + 1, 0), col_pos;
   for (size_t p = 0; p < n_bcols; ++p) if (cols[p] >= 0) col_ptr[cols[p] + 1]++;
@@ -1541,21 +1649,6 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   // lanes per row: ~3 chunks of 4 nonzeros per lane keeps several gathers in flight
   c->lanes = pow2_clamp((c->nnz + std::max<long long>(c->m, 1) - 1) / std::max<long long>(c->m, 1) / 12, 4, 32);
   if (const char* ev = getenv("QPK_LANES")) c->lanes = pow2_clamp(atoi(ev), 1, 32);
-  {
-    // flat row tiles for the TMA-fed CSR rows kernel
-    std::vector<int4> rt;
-    long long r = 0;
-    while (r < c->m) {
-      const long long ra = r;
-      const int e0 = c->h_rp[r];
-      int rows = 0;
-      while (r < c->m && rows < QPK_TILE_R && c->h_rp[r + 1] - e0 <= QPK_TILE_E - 8) { ++r; ++rows; }
-      if (rows == 0) { rt.clear(); break; }         // a row wider than a tile: no TMA rows path
-      rt.push_back(make_int4((int)ra, (int)r, c->h_rp[ra], c->h_rp[r]));
-    }
-    c->n_rtiles = (int)rt.size();
-    if (c->n_rtiles) CUDA_TRY(upload(c->rtile_desc, rt, s));
-  }
   // B'z strategy.  AUTO: the row-block dictionary when blocks reuse their
   // columns (banded / clustered B: RT, SVM, dense), else one-pass atomics
   // (random B, where no blocking creates reuse).  CSC and DICT are
@@ -1889,26 +1982,8 @@ int qpk_apply_dev(qpk_ctx* c, const double* v, double* y) {
 }  // extern "C"
 
 // ------------------------------------------------------------ slot engine ---
-static bool use_tma_rows(const qpk_ctx* c) {
-  if (c->n_rtiles <= 0) return false;
-  if (c->tma_rows >= 0) return c->tma_rows == 1;
-  const char* ev = getenv("QPK_TMA_ROWS");           // experimental: off unless asked for
-  return ev ? atoi(ev) == 1 : false;
-}
-
 template <int L, bool CSC>
 static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const Engine& E, int par) {
-  if (use_tma_rows(c)) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_slot_rows_tma_csr<L, CSC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)sizeof(CsrSmem));
-      attr = true;
-    }
-    k_slot_rows_tma_csr<L, CSC><<<E.G_rows, (QPK_CSR_WARPS + 1) * 32, sizeof(CsrSmem), s>>>(E, c->rtile_desc.p,
-                                                                                          c->n_rtiles, par);
-    return;
-  }
   k_slot_rows<L, CSC><<<grid, QPK_BLOCK, 0, s>>>(E, par);
 }
 
@@ -2050,7 +2125,7 @@ static Engine make_engine(qpk_ctx* c) {
   for (int i = 0; i < 3; ++i) E.x[i] = c->x[i].p;
   E.r = c->r.p; E.p = c->p.p; E.y = c->y.p; E.zb = c->zb.p; E.minv = c->minv.p;
   E.part = c->part.p; E.G = c->grid_eng;
-  E.G_rows = (c->scatter == QPK_SCATTER_DICT || use_tma_rows(c)) ? std::min(c->sms, c->grid_eng) : c->grid_eng;
+  E.G_rows = c->scatter == QPK_SCATTER_DICT ? std::min(c->sms, c->grid_eng) : c->grid_eng;
   if (c->scatter == QPK_SCATTER_PANEL) E.G_rows = c->panel_grid;
   E.panel.kp = c->panel_kp; E.panel.ew = c->panel_ew; E.panel.direct = c->panel_direct; E.panel.G = c->panel_grid;
   E.panel.P = c->panel_P.p; E.panel.pcols = c->panel_cols.p; E.panel.eci = c->panel_eci.p; E.panel.ev = c->panel_ev.p;

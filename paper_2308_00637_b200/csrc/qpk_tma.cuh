@@ -2,16 +2,9 @@
 // mbarrier::complete_tx; SASS UBLKCP) from HBM into a ring of shared-memory
 // stages, filled by one producer lane and drained by consumer warps.
 //   k_slot_rows_tile     dense-tile apply for clustered B (one pass, no atomics)
-//   k_slot_rows_tma_csr  CSR apply with the indices staged in shared memory
-//                        (experimental; QPK_TMA_ROWS=1)
 #pragma once
 #include "qpk_engine.cuh"
 
-#ifndef QPK_TMA_STAGES
-#define QPK_TMA_STAGES 4
-#endif
-#define QPK_TILE_E 2048          // max padded entries per tile
-#define QPK_TILE_R 256           // max rows per tile
 
 namespace qpk {
 
@@ -62,17 +55,6 @@ __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
-
-// tile descriptor written by the producer into its stage (visible to the
-// consumers through the mbarrier's release/acquire)
-struct TileDesc {
-  int ra, rb;           // rows
-  int e0;               // first entry copied for indices
-  int e1;               // first entry copied for values (multiple of 2)
-  int p0;               // first row pointer copied (multiple of 4)
-  int v0;               // first row copied for d (multiple of 2)
-  int w0;               // first element copied of the bottom vectors (n + row, multiple of 2)
-};
 
 __device__ __forceinline__ uint32_t round_up16(uint32_t b) { return b == 0u ? 16u : (b + 15u) & ~15u; }
 
@@ -594,178 +576,6 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_jac_tile(Engine E) {
       D.bpart[td.d0 + cc] = s0;
     }
   }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-fed CSR rows kernel (random / general B): the producer streams tiles of
-// the padded CSR (int32 columns + values) and the tile's per-row vectors into
-// shared memory; consumer sub-warps (L lanes per row, RB rows in flight per
-// sub-warp) read their indices from shared memory, so the u gathers -- the
-// random L2 requests that bound this kernel -- issue back to back instead of
-// waiting on a DRAM round trip for the indices.  CSC == true stores z_B for
-// the gather pass (deterministic); otherwise B'z is scattered with atomics.
-#define QPK_CSR_WARPS 16
-
-struct alignas(16) CsrStage {
-  int ci[QPK_TILE_E + 8];
-  double val[QPK_TILE_E + 8];
-  int rp[QPK_TILE_R + 8];
-  double d[QPK_TILE_R + 4];
-  double w[QPK_TILE_R + 4];
-  double r[QPK_TILE_R + 4];
-  double x[QPK_TILE_R + 4];
-  TileDesc t;
-};
-
-struct CsrSmem {
-  CsrStage st[QPK_TMA_STAGES];
-  unsigned long long full[QPK_TMA_STAGES], empty[QPK_TMA_STAGES];
-  double red[32];
-  double s_lr[QPK_KMAX];
-};
-
-template <int L, bool CSC>
-__global__ void __launch_bounds__((QPK_CSR_WARPS + 1) * 32, 1)
-k_slot_rows_tma_csr(Engine E, const int4* __restrict__ tdesc, int ntiles, int par) {
-  extern __shared__ __align__(128) unsigned char smraw[];
-  CsrSmem& S = *reinterpret_cast<CsrSmem*>(smraw);
-  const Ctrl c = E.ctrl[par];
-  if (c.mode == MODE_DONE) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) E.ctrl[par].t_rows = globaltimer_ns();
-  const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
-  double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
-  const Op& op = E.op;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < QPK_TMA_STAGES; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.empty[s], QPK_CSR_WARPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  double pacc = 0.0, rzb = 0.0;
-  const int my_tiles = (ntiles > (int)blockIdx.x) ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  if (warp == QPK_CSR_WARPS) {
-    const double* wsrc = v;
-    const double* xsrc = E.x[c.cur];
-    for (int base = 0; base < my_tiles; base += 32) {
-      int4 dsc = make_int4(0, 0, 0, 0);
-      if (base + lane < my_tiles) dsc = __ldg(tdesc + blockIdx.x + (size_t)(base + lane) * gridDim.x);
-      const int cnt = min(32, my_tiles - base);
-      for (int i = 0; i < cnt; ++i) {
-        const int it = base + i;
-        const int ra = __shfl_sync(0xffffffffu, dsc.x, i), rb = __shfl_sync(0xffffffffu, dsc.y, i);
-        const int ea = __shfl_sync(0xffffffffu, dsc.z, i), eb = __shfl_sync(0xffffffffu, dsc.w, i);
-        const int s = it % QPK_TMA_STAGES;
-        mbar_wait(&S.empty[s], ((it / QPK_TMA_STAGES) & 1) ^ 1);
-        if (lane == 0) {
-          CsrStage& st = S.st[s];
-          TileDesc td;
-          td.ra = ra; td.rb = rb;
-          td.e0 = ea & ~3;
-          td.e1 = ea & ~1;
-          td.p0 = ra & ~3;
-          td.v0 = ra & ~1;
-          td.w0 = (op.n + ra) & ~1;
-          st.t = td;
-          const uint32_t b_ci = round_up16((uint32_t)(((eb + 3) & ~3) - td.e0) * 4u);
-          const uint32_t b_val = round_up16((uint32_t)(((eb + 1) & ~1) - td.e1) * 8u);
-          const uint32_t b_rp = round_up16((uint32_t)(((rb + 1 + 3) & ~3) - td.p0) * 4u);
-          const uint32_t b_d = round_up16((uint32_t)(((rb + 1) & ~1) - td.v0) * 8u);
-          const uint32_t b_w = round_up16((uint32_t)(((op.n + rb + 1) & ~1) - td.w0) * 8u);
-          mbar_expect_tx(&S.full[s], b_ci + b_val + b_rp + b_d + b_w + (fuse ? 2 * b_w : 0u));
-          bulk_g2s(st.ci, op.ci + td.e0, b_ci, &S.full[s]);
-          bulk_g2s(st.val, op.bv + td.e1, b_val, &S.full[s]);
-          bulk_g2s(st.rp, op.rp + td.p0, b_rp, &S.full[s]);
-          bulk_g2s(st.d, op.d + td.v0, b_d, &S.full[s]);
-          bulk_g2s(st.w, wsrc + td.w0, b_w, &S.full[s]);
-          if (fuse) {
-            bulk_g2s(st.r, E.r + td.w0, b_w, &S.full[s]);
-            bulk_g2s(st.x, xsrc + td.w0, b_w, &S.full[s]);
-          }
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const double* u = v;
-    double* w = v + op.n;
-    constexpr int RPW = 32 / L;                      // rows per warp per step
-    constexpr int RB = 2;                            // steps in flight per sub-warp
-    const int sub = lane / L, ln = lane & (L - 1);
-    for (int it = 0; it < my_tiles; ++it) {
-      const int s = it % QPK_TMA_STAGES;
-      mbar_wait(&S.full[s], (it / QPK_TMA_STAGES) & 1);
-      const CsrStage& st = S.st[s];
-      const TileDesc td = st.t;
-      for (int r0 = td.ra + warp * RPW + sub; r0 - sub < td.rb; r0 += RB * QPK_CSR_WARPS * RPW) {
-        int b[RB], e[RB];
-        double sacc[RB];
-        int tmax = 0;
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-          const int r = r0 + q * QPK_CSR_WARPS * RPW;
-          b[q] = 0; e[q] = 0; sacc[q] = 0.0;
-          if (r < td.rb) { b[q] = st.rp[r - td.p0]; e[q] = st.rp[r + 1 - td.p0]; tmax = max(tmax, e[q] - b[q]); }
-        }
-        // uniform trip count across the warp (shuffles below need every lane)
-        for (int o = L; o < 32; o <<= 1) tmax = max(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
-        for (int j = ln; j < tmax; j += L) {
-#pragma unroll
-          for (int q = 0; q < RB; ++q) {
-            const int k = b[q] + j;
-            if (k < e[q]) {
-              const int col = st.ci[k - td.e0];
-              if (col >= 0) sacc[q] = fma(st.val[k - td.e1], u[col], sacc[q]);
-            }
-          }
-        }
-#pragma unroll
-        for (int o = L / 2; o > 0; o >>= 1)
-#pragma unroll
-          for (int q = 0; q < RB; ++q) sacc[q] += __shfl_xor_sync(0xffffffffu, sacc[q], o);
-#pragma unroll
-        for (int q = 0; q < RB; ++q) {
-          const int r = r0 + q * QPK_CSR_WARPS * RPW;
-          if (r >= td.rb) continue;
-          const double tt = sacc[q];
-          const double dr = st.d[r - td.v0];
-          double wv = st.w[op.n + r - td.w0];
-          if (fuse) {
-            const double rres = st.r[op.n + r - td.w0];
-            const double zr = __dmul_rn(1.0 / dr, rres);
-            if (c.xupd && ln == 0)
-              E.x[c.xn][op.n + r] = __dadd_rn(st.x[op.n + r - td.w0], __dmul_rn(c.alpha_prev, wv));
-            const double pn = (c.mode == MODE_RESTART) ? zr : __dadd_rn(zr, __dmul_rn(c.beta, wv));
-            if (ln == 0) { w[r] = pn; rzb += rres * zr; }
-            wv = pn;
-          }
-          const double z = __dadd_rn(__ddiv_rn(__dmul_rn(2.0, tt), dr), wv);
-          const double yb = __dadd_rn(tt, __dmul_rn(dr, wv));
-          if (ln == 0) {
-            E.y[op.n + r] = yb;
-            pacc += tt * z + wv * yb;
-            if (CSC) E.zb[r] = z;
-          }
-          if (!CSC) {
-            for (int k = b[q] + ln; k < e[q]; k += L) {
-              const int col = st.ci[k - td.e0];
-              if (col >= 0) atomicAdd(E.y + col, z * st.val[k - td.e1]);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&S.empty[s]);
-    }
-  }
-  __syncthreads();
-  pacc += hess_rows(op, v, E.y, E.part, E.G, S.red, S.s_lr);
-  double t = block_sum(pacc, S.red);
-  if (threadIdx.x == 0) E.part[SLOT_ROWS * E.G + blockIdx.x] = t;
-  t = block_sum(rzb, S.red);
-  if (threadIdx.x == 0) E.part[SLOT_AUX2 * E.G + blockIdx.x] = t;
 }
 
 }  // namespace qpk

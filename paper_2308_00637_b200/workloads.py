@@ -110,11 +110,13 @@ def rt_like(seed: int = 3, n_vox: int = 200_000, n_beam: int = 20_000, density: 
     starts = rng.integers(0, n_vox - band + 1, size=n_beam)
     r = np.arange(band, dtype=np.float64)
     vals = np.exp(-r / 5.0)[None, :] * rng.uniform(0.5, 1.0, size=(n_beam, band))
+    # column j holds the rows starts[j] .. starts[j] + band - 1 (no duplicates):
+    # that IS a CSC matrix; its CSR conversion is one counting pass and leaves
+    # the column indices of every row sorted (same arrays as building it from
+    # COO triplets, without their sort)
     rows = starts[:, None] + np.arange(band)[None, :]
-    cols = np.repeat(np.arange(n_beam), band)
-    dmat = sp.csr_matrix((vals.ravel(), (rows.ravel(), cols)), shape=(n_vox, n_beam))
-    dmat.sum_duplicates()
-    dmat.sort_indices()
+    dmat = sp.csc_matrix((vals.ravel(), rows.ravel(), np.arange(n_beam + 1, dtype=np.int64) * band),
+                         shape=(n_vox, n_beam)).tocsr()
     n_t = int(round(target_frac * n_vox))
     d_t = dmat[:n_t]
     d_oar = dmat[n_t:].tocsr()
