@@ -296,6 +296,11 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_hess(Op op, const double* u, doub
   else hess_rows(op, u, y, part, G, red, s_lr);
 }
 
+// the packed symmetric H's partials into y (after k_hess), fixed order
+__global__ void __launch_bounds__(QPK_BLOCK) k_sym_combine(Op op, const double* u, double* y) {
+  sym_combine(op, u, y);
+}
+
 // dense symmetric H -> its upper 64 x 64 tiles, tile (I, J >= I) at
 // I*nt - I*(I-1)/2 + (J - I), zero padded past n
 __global__ void __launch_bounds__(256) k_pack_sym(const double* __restrict__ Hd, long long n, int nt,
@@ -515,6 +520,17 @@ static void parallel_chunks(int nchunks, F fn) {
   for (auto& t : th) t.join();
 }
 
+struct SetupTimer {
+  bool on = getenv("QPK_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[qpk setup] %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 constexpr int NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
 }  // namespace
@@ -574,6 +590,8 @@ struct qpk_ctx {
   int n_dense = 0;
   DBuf<int4> hchunks;
   int h_nchunks = 0;
+  DBuf<double> hsymp;            // partial sums of the packed symmetric apply
+  DBuf<int> hrowchunk;
   bool have_csc = false;
   // dense column panel (QPK_SCATTER_PANEL)
   bool have_panel = false;
@@ -635,6 +653,7 @@ struct qpk_ctx {
     o.H.kind = hkind; o.H.h = hh.p; o.H.rp = hrp.p; o.H.ci = hci.p; o.H.v = hv.p; o.H.lanes = h_lanes;
     o.H.dense = hdense.p; o.H.U = U.p; o.H.w = w.p; o.H.k = (int)hk;
     o.H.sym = hsym.p; o.H.chunks = hchunks.p; o.H.nchunks = h_nchunks;
+    o.H.symp = hsymp.p; o.H.rowchunk = hrowchunk.p;
     o.H.rows = h_own_set ? hown.p : nullptr; o.H.nrows = h_own_set ? (int)h_own.size() : 0;
     o.d = d.p; o.q = q.p;
     o.top_owner = rank == 0 ? 1 : 0;
@@ -1155,12 +1174,13 @@ static void tile_range(const int* rp, const int* ci, const double* v, const int*
 // the tile storage would exceed the int32 offsets).
 static long long tile_rows_parallel(const int* rp, const int* ci, const double* v, const int* perm, long long nrows,
                                     int kind, long long n, std::vector<TileDescD>& tiles, std::vector<int>& cols,
-                                    std::vector<double>& tval) {
+                                    std::vector<double>& tval, size_t reserve_extra = 0) {
   if (nrows <= 0) return 0;
-  int C = perm ? 1 : (int)std::max<long long>(1, std::min<long long>(512, nrows / 2048));
+  const int C = (int)std::max<long long>(1, std::min<long long>(512, nrows / 2048));
   std::vector<long long> cut(C + 1, 0);
   cut[C] = nrows;
   for (int k = 1; k < C; ++k) {
+    if (perm) { cut[k] = nrows * k / C; continue; }   // permuted rows: equal row counts
     const long long want = (long long)rp[0] + ((long long)rp[nrows] - rp[0]) * k / C;
     cut[k] = std::max(cut[k - 1], (long long)(std::lower_bound(rp, rp + nrows, (int)want) - rp));
   }
@@ -1194,6 +1214,10 @@ static long long tile_rows_parallel(const int* rp, const int* ci, const double* 
     tb[k + 1] = tb[k] + outs[k].tiles.size();
   }
   if (vb[C] >= (size_t)(1LL << 31) - 64 || cb[C] >= (size_t)(1LL << 31) - 64) return -1;
+  // (room for what the caller appends next -- the Hessian tiles -- so the
+  // 1.4 GB value array of cfg4 is not reallocated and copied)
+  cols.reserve(cb[C] + reserve_extra + 64);
+  tval.reserve(vb[C] + reserve_extra + 64);
   cols.resize(cb[C]);
   tval.resize(vb[C], 0.0);
   tiles.resize(tb[C]);
@@ -1237,10 +1261,13 @@ static int build_dict(qpk_ctx* c, bool probe) {
   }
   auto tile_rows = [&](const int* rp, const int* ci, const double* v, long long nrows, int kind,
                        const int* perm) -> long long {
-    return tile_rows_parallel(rp, ci, v, perm, nrows, kind, n, tiles, cols, tval);
+    return tile_rows_parallel(rp, ci, v, perm, nrows, kind, n, tiles, cols, tval,
+                              kind == 0 && c->hkind == QPK_HESS_CSR ? 2 * c->h_hci.size() + 65536 : 0);
   };
+  SetupTimer tm;
   const long long slots = tile_rows(c->h_rp.data(), c->h_ci.data(), c->h_v.data(), m, 0, nullptr);
   if (slots < 0) return QPK_OK;                       // a row wider than a tile
+  tm.lap("  B tiles");
   int tid = (int)tiles.size();
   const size_t n_bcols = cols.size();
   const int n_btiles = tid;
@@ -1276,6 +1303,7 @@ static int build_dict(qpk_ctx* c, bool probe) {
     }
   }
   tid = (int)tiles.size();
+  tm.lap("  H tiles");
   // column -> its B-tile-partial positions, in tile order
   std::vector<int> col_ptr(n + 1, 0), col_pos;
   for (size_t p = 0; p < n_bcols; ++p) if (cols[p] >= 0) col_ptr[cols[p] + 1]++;
@@ -1302,6 +1330,7 @@ static int build_dict(qpk_ctx* c, bool probe) {
     CUDA_TRY(c->comb_sum.alloc(std::max(c->comb_nseg, 1)));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
   }
+  tm.lap("  col index");
   // CTA-level accumulation: CTA b runs a consecutive, slot-balanced range of
   // tiles and sums their partials per column of the range's union in shared
   // memory; the combine then reads ~one partial per (CTA, column)
@@ -1369,6 +1398,7 @@ static int build_dict(qpk_ctx* c, bool probe) {
       c->tile_grid = G;
     }
   }
+  tm.lap("  CTA slots");
   cols.resize(cols.size() + 16, -1);                  // bulk copies read 16-byte windows
   tval.resize(tval.size() + 16, 0.0);
   cudaStream_t s = c->stream;
@@ -1379,6 +1409,7 @@ static int build_dict(qpk_ctx* c, bool probe) {
   CUDA_TRY(upload(c->col_pos, col_pos, s));
   CUDA_TRY(c->bpart.alloc(std::max<size_t>(cols.size(), 1)));
   CUDA_TRY(cudaStreamSynchronize(s));
+  tm.lap("  tile upload");
   c->nblk = tid;
   c->dict_reuse = slots ? (double)c->nnz / (double)slots : 0.0;
   c->have_dict = true;
@@ -1590,17 +1621,6 @@ static int build_cluster(qpk_ctx* c) {
 }
 
 // QPK_TIMING=1: host setup phases of qpk_problem_finalize on stderr
-struct SetupTimer {
-  bool on = getenv("QPK_TIMING") != nullptr;
-  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
-  void lap(const char* what) {
-    if (!on) return;
-    const auto now = std::chrono::steady_clock::now();
-    fprintf(stderr, "[qpk setup] %-12s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
-    t = now;
-  }
-};
-
 int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   SetupTimer tm;
   if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_finalize: no problem being built");
@@ -1767,12 +1787,17 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     k_pack_sym<<<dim3(nt, nt), 256, 0, s>>>(c->hdense.p, c->n, nt, c->hsym.p);
     c->launches++;
     std::vector<int4> ch;
+    std::vector<int> rowchunk(nt + 1, 0);
     for (int I = 0; I < nt; ++I) {
       const int base = (int)((size_t)I * nt - (size_t)I * (I - 1) / 2);
+      rowchunk[I] = (int)ch.size();
       for (int J0 = I; J0 < nt; J0 += QPK_SYM_CHUNK)
         ch.push_back(make_int4(I, J0, std::min(J0 + QPK_SYM_CHUNK, nt), base + (J0 - I)));
     }
+    rowchunk[nt] = (int)ch.size();
     CUDA_TRY(upload(c->hchunks, ch, s));
+    CUDA_TRY(upload(c->hrowchunk, rowchunk, s));
+    CUDA_TRY(c->hsymp.alloc((ch.size() + tiles) * 64));
     c->h_nchunks = (int)ch.size();
   }
   // leading dense rows of B (the SVM dual's y' alpha = 0): as dense vectors,
@@ -1922,7 +1947,11 @@ static int apply_impl(qpk_ctx* c, const double* v_dev, double* y_dev) {
   else launch_rows<false>(c->lanes, G, s, o, v_dev, y_dev, c->zb.p, c->part.p, G);
   c->launches += 2;
   if (csc) { k_finish_csc<<<G, QPK_BLOCK, 0, s>>>(o, y_dev, c->zb.p); c->launches++; }
-  if (c->h_nchunks) { k_hess<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev, c->part.p, G); c->launches++; }
+  if (c->h_nchunks) {
+    k_hess<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev, c->part.p, G);
+    k_sym_combine<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev);
+    c->launches += 2;
+  }
   CUDA_TRY(cudaGetLastError());
   return allreduce_sum(c, y_dev, c->n, s);          // sharded: y_top = sum of the ranks' partials
 }
@@ -2012,9 +2041,11 @@ static bool slot_csc(const qpk_ctx* c) {
 static int slot_launches(const qpk_ctx* c) {
   int k = 2;                                                    // top, update
   if (c->scatter == QPK_SCATTER_DICT)
-    k += (comb_fused(c) ? 1 : comb_direct(c) ? 2 : 3) + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0);
-  else if (c->scatter == QPK_SCATTER_PANEL) k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0);
-  else k += 1 + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 1 : 0) + (c->n_dense ? 1 : 0);
+    k += (comb_fused(c) ? 1 : comb_direct(c) ? 2 : 3) + ((c->hkind != QPK_HESS_DIAG && !c->h_tiled) ? 1 : 0) +
+         (c->h_nchunks ? 1 : 0);
+  else if (c->scatter == QPK_SCATTER_PANEL)
+    k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 1 : 0);
+  else k += 1 + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 2 : 0) + (c->n_dense ? 1 : 0);
   if (c->sharded) k += 2;
   return k;
 }
@@ -2033,6 +2064,7 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
                                ? (int)std::min<long long>(2 * c->sms, (c->m * c->panel_ew + 1023) / 1024) : 0;
     launch_k(pdl, k_panel_comb, dim3(c->panel_kp / 32 + rem_blocks), dim3(1024), 0, s, E, c->y.p, 1, par);
     if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    if (c->h_nchunks) k_slot_sym_combine<<<G, QPK_BLOCK, 0, s>>>(E, par);
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   } else if (c->scatter == QPK_SCATTER_DICT) {
     launch_k(pdl, k_slot_rows_tile, dim3(E.G_rows),
@@ -2047,6 +2079,7 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
       launch_k(pdl, k_comb_col, dim3(G), dim3(QPK_BLOCK), 0, s, E, c->y.p, 1, par);
     }
     if (c->hkind != QPK_HESS_DIAG && !c->h_tiled) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    if (c->h_nchunks) k_slot_sym_combine<<<G, QPK_BLOCK, 0, s>>>(E, par);
   } else {
     switch (c->lanes * 2 + (csc ? 1 : 0)) {
       case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
@@ -2067,8 +2100,10 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
       else k_slot_dense<false><<<G, QPK_BLOCK, 0, s>>>(E, par);
     }
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
-    if (c->h_nchunks)                                                  // packed symmetric dense H
+    if (c->h_nchunks) {                                                // packed symmetric dense H
       k_slot_hess_sym<<<QPK_SYM_MINB * c->sms, QPK_BLOCK, 0, s>>>(E, par);
+      k_slot_sym_combine<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    }
   }
 }
 
@@ -2455,6 +2490,7 @@ static void ipm_hess_apply(qpk_ctx* c, const double* xv, double* out) {
   const int G = c->grid_std;
   k_prep<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out, c->part.p, G);
   k_hess<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out, c->part.p, G);
+  if (c->h_nchunks) { k_sym_combine<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out); c->launches++; }
   c->launches += 2;
 }
 

@@ -34,6 +34,9 @@ struct Hess {
   const double* sym;                    // dense H as packed upper 64 x 64 tiles (null: not built)
   const int4* chunks;                   // sym work units {I, J0, J1, tile of (I, J0)}
   int nchunks;
+  double* symp;                         // sym partials, 64 doubles each: [unit ch] its tile-row sums, then
+                                        // [nchunks + tile t] the column sums of off-diagonal tile t
+  const int* rowchunk;                  // units of tile row I: [rowchunk[I], rowchunk[I+1])
   const double* U; const double* w; int k;                  // LOWRANK: U n x k row-major
 };
 
@@ -328,8 +331,9 @@ __device__ __forceinline__ double hess_rows(const Op& op, const double* u, doubl
 //   rows:     (H_IJ u_J)_r needs a sum over lanes: 32 rows at a time, a
 //             transposed butterfly (31 shuffles) leaves row r0+l in lane l;
 //             accumulated over the unit's tiles -> y_I
-// Partial sums are added with fp64 atomics (like the row-major dense path);
-// returns this thread's share of u'H u.
+// No atomics: every unit stores its 64 row sums and every off-diagonal tile its
+// 64 column sums as partials (op.H.symp); sym_combine adds them into y in a
+// fixed order (bitwise reproducible) and returns u'H u.
 template <int RG>
 __device__ __forceinline__ double hess_sym_t(const Op& op, const double* u, double* y) {
   if (!op.top_owner) return 0.0;
@@ -382,13 +386,42 @@ __device__ __forceinline__ double hess_sym_t(const Op& op, const double* u, doub
         if (row == lane) ry0 += p[0];
         else if (row == 32 + lane) ry1 += p[0];
       }
-      if (J != cd.x) {
-        if (cJ < n) { atomicAdd(y + cJ, cz0); acc += uJx * cz0; }
-        if (cJ + 1 < n) { atomicAdd(y + cJ + 1, cz1); acc += uJy * cz1; }
-      }
+      if (J != cd.x)
+        reinterpret_cast<double2*>(op.H.symp + ((size_t)op.H.nchunks + t) * 64)[lane] = make_double2(cz0, cz1);
     }
-    if (rI + lane < n) { atomicAdd(y + rI + lane, ry0); acc += uI0 * ry0; }
-    if (rI + 32 + lane < n) { atomicAdd(y + rI + 32 + lane, ry1); acc += uI1 * ry1; }
+    double* rp_ = op.H.symp + (size_t)ch * 64;
+    rp_[lane] = ry0;
+    rp_[32 + lane] = ry1;
+  }
+  return acc;
+}
+
+// y_j += (H u)_j from the partials of hess_sym_t, in a fixed order: the units
+// of tile row J = j / 64 (their row sums), then the column sums of the tiles
+// (I, J), I = 0 .. J-1.  Returns this thread's share of u'H u.
+__device__ __forceinline__ double sym_combine(const Op& op, const double* u, double* y) {
+  const int n = op.n, nt = (n + 63) >> 6;
+  double acc = 0.0;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const int J = j >> 6, cc = j & 63;
+    double s = 0.0;
+    for (int ch = __ldg(op.H.rowchunk + J), e = __ldg(op.H.rowchunk + J + 1); ch < e; ++ch)
+      s += op.H.symp[(size_t)ch * 64 + cc];
+    const double* cp = op.H.symp + (size_t)op.H.nchunks * 64 + cc;
+    int I = 0;
+    for (; I + 3 < J; I += 4) {                        // tile (I, J) is tile I nt - I (I - 1) / 2 + (J - I)
+      double p4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const size_t t = (size_t)(I + q) * nt - (size_t)(I + q) * (I + q - 1) / 2 + (J - I - q);
+        p4[q] = cp[t * 64];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) s += p4[q];
+    }
+    for (; I < J; ++I) s += cp[((size_t)I * nt - (size_t)I * (I - 1) / 2 + (J - I)) * 64];
+    y[j] += s;
+    acc += u[j] * s;
   }
   return acc;
 }

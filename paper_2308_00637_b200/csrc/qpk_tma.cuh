@@ -488,15 +488,23 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_hess(Engine E, int par) {
 #define QPK_SYM_MINB 1            // blocks per SM (RG 32: ~250 registers; measured best of RG 16/32 x 1/2)
 #endif
 __global__ void __launch_bounds__(QPK_BLOCK, QPK_SYM_MINB) k_slot_hess_sym(Engine E, int par) {
+  const Ctrl c = E.ctrl[par];
+  if (c.mode == MODE_DONE) return;
+  const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
+  const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
+  hess_sym_t<QPK_SYM_RG>(E.op, v, E.y);              // partials only; k_slot_sym_combine adds them into y
+}
+
+// the packed symmetric H's partials summed into y_top in a fixed order, u'H u
+// into the slot's PREP partials (grid <= E.G, one partial slot per block)
+__global__ void __launch_bounds__(QPK_BLOCK) k_slot_sym_combine(Engine E, int par) {
   __shared__ double red[32];
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
   const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
   const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
-  const double acc = hess_sym_t<QPK_SYM_RG>(E.op, v, E.y);
-  const double t = block_sum(acc, red);
-  // the grid is sized for the matrix stream, not for the slot's partial layout
-  if (threadIdx.x == 0) atomicAdd(E.part + SLOT_PREP * E.G + blockIdx.x % E.G, t);
+  const double t = block_sum(sym_combine(E.op, v, E.y), red);
+  if (threadIdx.x == 0) E.part[SLOT_PREP * E.G + blockIdx.x] += t;
 }
 
 // Column sums of the B-tile partials in two deterministic levels, balanced for

@@ -35,7 +35,18 @@ class GpuKkt:
     """Device-resident doubly augmented operator of one QpProblem."""
 
     def __init__(self, problem, bmap, device: int = 0, scatter: int = _native.QPK_SCATTER_AUTO):
+        import time
+        t0 = time.perf_counter()
+        timing = bool(os.environ.get("QPK_TIMING"))
+
+        def lap(what):
+            nonlocal t0
+            if timing:
+                t1 = time.perf_counter()
+                print(f"[qpk setup] py {what:<12s} {(t1 - t0) * 1e3:8.1f} ms", file=sys.stderr, flush=True)
+                t0 = t1
         self.ctx = _native.Context(device)
+        lap("context")
         self.n = int(problem.n)
         lin_lower = np.ascontiguousarray(bmap.lin_lower, dtype=np.int64)
         lin_upper = np.ascontiguousarray(bmap.lin_upper, dtype=np.int64)
@@ -57,9 +68,12 @@ class GpuKkt:
                 if len(rows):
                     c.call("qpk_problem_add_rows", int(am.n_rows), _native.ptr(ro), _native.ptr(ci),
                            _native.ptr(v), _native.ptr(rows), len(rows), sign)
+        lap("add_rows")
         self._set_hessian(problem.hessian)
+        lap("hessian")
         # AUTO lets the library pick per matrix (QPK_SCATTER in the environment overrides)
         c.call("qpk_problem_finalize", int(scatter))
+        lap("finalize")
         self._hist = None
 
     def _set_hessian(self, h):

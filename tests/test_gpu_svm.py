@@ -128,6 +128,50 @@ def test_packed_symmetric_hessian_apply():
     env = parity.envelope(op_h, rhs, cfg_p, h_ref)
     ok, msg = parity.check_history(hist, h_ref, env)
     assert ok, msg
+    # no atomics on this path: partials are summed in a fixed order
+    xg2, _, hist2 = gk.pcg(rhs, 1e-300, 40, True, history=True)
+    np.testing.assert_array_equal(xg, xg2)
+    np.testing.assert_array_equal(hist, hist2)
+    np.testing.assert_array_equal(gk.apply(v), gk.apply(v))
+    gk.close()
+
+
+def test_unsymmetric_dense_hessian_is_not_packed():
+    """DenseHessian documents symmetry but the reference multiplies whatever it
+    is given (model.py:165-176: h.m @ v).  A dense H that is not bitwise
+    symmetric must keep the row-major apply, not the mirrored upper triangle."""
+    from oracle import qp_oracle as orc
+    from paper_2308_00637_b200.direction import GpuKkt
+    from paper_2308_00637_b200.problem import (Bounds, DenseHessian, IterateState, QpProblem, SparseMatrix,
+                                               build_operator)
+    rng = np.random.default_rng(31)
+    n = 640
+    g = rng.standard_normal((n, n))
+    h = g @ g.T + n * np.eye(n)
+    h[3, 500] += 0.25                                    # one entry off: H != H'
+    problem = QpProblem(n=n, hessian=DenseHessian(h), p=np.zeros(n), a=SparseMatrix.empty(0, n),
+                        lin_bounds=Bounds.free(0), c=SparseMatrix.empty(0, n), b=[], var_bounds=Bounds.free(n))
+    z = np.zeros(0)
+    state = IterateState(x=np.zeros(n), s_lA=z, s_uA=z, s_lx=z, s_ux=z, lam_e=z, lam_lA=z, lam_uA=z, lam_lx=z,
+                         lam_ux=z, mu=0.5)
+    op = build_operator(problem, state)
+    gk = GpuKkt(problem, op.bmap)
+    assert gk.ctx.query("hess_symmetric") == 0 and gk.ctx.query("hess_sym") == 0
+    gk.set_diagonals(op.d_diag, op.q_diag_extra)
+    v = rng.standard_normal(n)
+    y_ref = orc.apply_doubly_augmented(op, v)
+    assert np.linalg.norm(gk.apply(v) - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
+    gk.close()
+    h[3, 500] -= 0.25
+    h = 0.5 * (h + h.T)
+    problem = QpProblem(n=n, hessian=DenseHessian(h), p=np.zeros(n), a=SparseMatrix.empty(0, n),
+                        lin_bounds=Bounds.free(0), c=SparseMatrix.empty(0, n), b=[], var_bounds=Bounds.free(n))
+    op = build_operator(problem, state)
+    gk = GpuKkt(problem, op.bmap)
+    assert gk.ctx.query("hess_symmetric") == 1 and gk.ctx.query("hess_sym") == 1
+    gk.set_diagonals(op.d_diag, op.q_diag_extra)
+    y_ref = orc.apply_doubly_augmented(op, v)
+    assert np.linalg.norm(gk.apply(v) - y_ref) <= 1e-12 * np.linalg.norm(y_ref)
     gk.close()
 
 
