@@ -297,8 +297,9 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_hess(Op op, const double* u, doub
 }
 
 // the packed symmetric H's partials into y (after k_hess), fixed order
-__global__ void __launch_bounds__(QPK_BLOCK) k_sym_combine(Op op, const double* u, double* y) {
-  sym_combine(op, u, y);
+__global__ void __launch_bounds__(QPK_SYMC_BLOCK) k_sym_combine(Op op, const double* u, double* y) {
+  __shared__ double sh[QPK_SYMC_BLOCK];
+  sym_combine(op, u, y, sh);
 }
 
 // dense symmetric H -> its upper 64 x 64 tiles, tile (I, J >= I) at
@@ -1949,7 +1950,7 @@ static int apply_impl(qpk_ctx* c, const double* v_dev, double* y_dev) {
   if (csc) { k_finish_csc<<<G, QPK_BLOCK, 0, s>>>(o, y_dev, c->zb.p); c->launches++; }
   if (c->h_nchunks) {
     k_hess<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev, c->part.p, G);
-    k_sym_combine<<<G, QPK_BLOCK, 0, s>>>(o, v_dev, y_dev);
+    k_sym_combine<<<G, QPK_SYMC_BLOCK, 0, s>>>(o, v_dev, y_dev);
     c->launches += 2;
   }
   CUDA_TRY(cudaGetLastError());
@@ -2064,7 +2065,7 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
                                ? (int)std::min<long long>(2 * c->sms, (c->m * c->panel_ew + 1023) / 1024) : 0;
     launch_k(pdl, k_panel_comb, dim3(c->panel_kp / 32 + rem_blocks), dim3(1024), 0, s, E, c->y.p, 1, par);
     if (c->hkind != QPK_HESS_DIAG) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
-    if (c->h_nchunks) k_slot_sym_combine<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    if (c->h_nchunks) k_slot_sym_combine<<<G, QPK_SYMC_BLOCK, 0, s>>>(E, par);
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
   } else if (c->scatter == QPK_SCATTER_DICT) {
     launch_k(pdl, k_slot_rows_tile, dim3(E.G_rows),
@@ -2079,7 +2080,7 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
       launch_k(pdl, k_comb_col, dim3(G), dim3(QPK_BLOCK), 0, s, E, c->y.p, 1, par);
     }
     if (c->hkind != QPK_HESS_DIAG && !c->h_tiled) k_slot_hess<<<G, QPK_BLOCK, 0, s>>>(E, par);
-    if (c->h_nchunks) k_slot_sym_combine<<<G, QPK_BLOCK, 0, s>>>(E, par);
+    if (c->h_nchunks) k_slot_sym_combine<<<G, QPK_SYMC_BLOCK, 0, s>>>(E, par);
   } else {
     switch (c->lanes * 2 + (csc ? 1 : 0)) {
       case 2: launch_slot_rows_t<1, false>(c, G, s, E, par); break;
@@ -2102,7 +2103,7 @@ static void launch_slot_apply(qpk_ctx* c, const Engine& E, int par, cudaStream_t
     if (csc) k_slot_csc<<<c->sms * 8, QPK_BLOCK, 0, s>>>(E, par);
     if (c->h_nchunks) {                                                // packed symmetric dense H
       k_slot_hess_sym<<<QPK_SYM_MINB * c->sms, QPK_BLOCK, 0, s>>>(E, par);
-      k_slot_sym_combine<<<G, QPK_BLOCK, 0, s>>>(E, par);
+      k_slot_sym_combine<<<G, QPK_SYMC_BLOCK, 0, s>>>(E, par);
     }
   }
 }
@@ -2490,7 +2491,7 @@ static void ipm_hess_apply(qpk_ctx* c, const double* xv, double* out) {
   const int G = c->grid_std;
   k_prep<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out, c->part.p, G);
   k_hess<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out, c->part.p, G);
-  if (c->h_nchunks) { k_sym_combine<<<G, QPK_BLOCK, 0, c->stream>>>(o, xv, out); c->launches++; }
+  if (c->h_nchunks) { k_sym_combine<<<G, QPK_SYMC_BLOCK, 0, c->stream>>>(o, xv, out); c->launches++; }
   c->launches += 2;
 }
 

@@ -396,32 +396,41 @@ __device__ __forceinline__ double hess_sym_t(const Op& op, const double* u, doub
   return acc;
 }
 
-// y_j += (H u)_j from the partials of hess_sym_t, in a fixed order: the units
-// of tile row J = j / 64 (their row sums), then the column sums of the tiles
-// (I, J), I = 0 .. J-1.  Returns this thread's share of u'H u.
-__device__ __forceinline__ double sym_combine(const Op& op, const double* u, double* y) {
+// y_j += (H u)_j from the partials of hess_sym_t, in a fixed order.  One block
+// per tile column J (grid-stride): its items are the units of tile row J (row
+// sums) followed by the tiles (I, J), I = 0 .. J-1 (column sums); thread
+// (cc = tid % 64, part = tid / 64) adds the items part, part + P, ... for
+// output 64 J + cc, the P parts are then added in order.  Returns this thread's
+// share of u'H u.  `sh` holds blockDim.x doubles.
+__device__ __forceinline__ double sym_combine(const Op& op, const double* u, double* y, double* sh) {
   const int n = op.n, nt = (n + 63) >> 6;
+  const int cc = threadIdx.x & 63, part = threadIdx.x >> 6, P = blockDim.x >> 6;
+  const double* rowp = op.H.symp + cc;
+  const double* colp = op.H.symp + (size_t)op.H.nchunks * 64 + cc;
   double acc = 0.0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const int J = j >> 6, cc = j & 63;
+  for (int J = blockIdx.x; J < nt; J += gridDim.x) {
+    const int c0 = __ldg(op.H.rowchunk + J), nrow = __ldg(op.H.rowchunk + J + 1) - c0, items = nrow + J;
+    auto item = [&](int k) -> double {
+      if (k < nrow) return rowp[(size_t)(c0 + k) * 64];
+      const int I = k - nrow;                          // tile (I, J) is tile I nt - I (I - 1) / 2 + (J - I)
+      return colp[((size_t)I * nt - (size_t)I * (I - 1) / 2 + (J - I)) * 64];
+    };
     double s = 0.0;
-    for (int ch = __ldg(op.H.rowchunk + J), e = __ldg(op.H.rowchunk + J + 1); ch < e; ++ch)
-      s += op.H.symp[(size_t)ch * 64 + cc];
-    const double* cp = op.H.symp + (size_t)op.H.nchunks * 64 + cc;
-    int I = 0;
-    for (; I + 3 < J; I += 4) {                        // tile (I, J) is tile I nt - I (I - 1) / 2 + (J - I)
-      double p4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const size_t t = (size_t)(I + q) * nt - (size_t)(I + q) * (I + q - 1) / 2 + (J - I - q);
-        p4[q] = cp[t * 64];
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) s += p4[q];
+    int k = part;
+    for (; k + 3 * P < items; k += 4 * P) {
+      const double a0 = item(k), a1 = item(k + P), a2 = item(k + 2 * P), a3 = item(k + 3 * P);
+      s += a0; s += a1; s += a2; s += a3;
     }
-    for (; I < J; ++I) s += cp[((size_t)I * nt - (size_t)I * (I - 1) / 2 + (J - I)) * 64];
-    y[j] += s;
-    acc += u[j] * s;
+    for (; k < items; k += P) s += item(k);
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    if (part == 0) {
+      double t = s;
+      for (int q = 1; q < P; ++q) t += sh[q * 64 + cc];
+      const int j = J * 64 + cc;
+      if (j < n) { y[j] += t; acc += u[j] * t; }
+    }
+    __syncthreads();
   }
   return acc;
 }

@@ -497,13 +497,15 @@ __global__ void __launch_bounds__(QPK_BLOCK, QPK_SYM_MINB) k_slot_hess_sym(Engin
 
 // the packed symmetric H's partials summed into y_top in a fixed order, u'H u
 // into the slot's PREP partials (grid <= E.G, one partial slot per block)
-__global__ void __launch_bounds__(QPK_BLOCK) k_slot_sym_combine(Engine E, int par) {
+#define QPK_SYMC_BLOCK 1024       // 16 parts per output: ~300 partials per output are summed in ~5 round trips
+__global__ void __launch_bounds__(QPK_SYMC_BLOCK) k_slot_sym_combine(Engine E, int par) {
   __shared__ double red[32];
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
   const bool fuse = c.mode == MODE_NORMAL || c.mode == MODE_RESTART;
   const double* v = fuse ? E.p : E.x[c.mode == MODE_CHECK ? c.xn : c.best];
-  const double t = block_sum(sym_combine(E.op, v, E.y), red);
+  __shared__ double sh[QPK_SYMC_BLOCK];
+  const double t = block_sum(sym_combine(E.op, v, E.y, sh), red);
   if (threadIdx.x == 0) E.part[SLOT_PREP * E.G + blockIdx.x] += t;
 }
 
