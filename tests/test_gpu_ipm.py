@@ -13,7 +13,7 @@ import golden_io
 from oracle import qp_oracle as orc
 from paper_2308_00637_b200 import workloads
 from paper_2308_00637_b200.direction import gpu_direction
-from paper_2308_00637_b200.pcg import PcgBreakdownError
+from paper_2308_00637_b200.pcg import PcgBreakdownError, result_types
 
 pytestmark = pytest.mark.gpu
 
@@ -33,7 +33,7 @@ def test_ipm_with_gpu_direction(name):
     else:
         problem = golden_io.problem_from(IPM, pre)
     cfg = cfg_from(IPM[pre + "cfg"])
-    rep = orc.solve(problem, cfg, direction_solver=gpu_direction, breakdown_types=(PcgBreakdownError,))
+    rep = orc.solve(problem, cfg, direction_solver=gpu_direction, breakdown_types=(PcgBreakdownError, result_types()[1]))
     assert rep.status == str(IPM[pre + "status"])
     obj = float(IPM[pre + "objective"])
     assert abs(rep.objective - obj) <= 1e-6 * max(abs(obj), 1.0)
