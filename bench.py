@@ -488,6 +488,11 @@ def run_ours(args):
     rows_kernel = {3: "k_slot_rows_tile", 4: "k_slot_panel"}.get(gk.ctx.query("scatter"), "k_slot_rows") \
         if engine_used else "pcg_kernel (rows phase)"
     fmt_bytes = gk.ctx.query("format_bytes")
+    if gk.ctx.query("hess_sym"):
+        # dense symmetric H as packed upper tiles: the operator pass is its stream (+ the partials)
+        rows_kernel = "k_slot_hess_sym + k_slot_sym_combine (packed symmetric H) + k_slot_rows / k_slot_dense"
+        nt = (op.n + 63) // 64
+        fmt_bytes += nt * (nt + 1) // 2 * 4096 * 8
     dom = {"name": rows_kernel, "us_per_iter": round(float(phases[1]), 2),
            "share_of_iteration": round(float(phases[1] / max(phases.sum(), 1e-9)), 3),
            "csr_matrix_bytes_per_iter": per_iter - 88 * op.dim,
