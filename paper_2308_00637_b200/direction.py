@@ -47,6 +47,14 @@ class GpuKkt:
                 t0 = t1
         self.ctx = _native.Context(device)
         lap("context")
+        self._upload(problem, bmap, scatter, lap)
+
+    def reload(self, problem, bmap, scatter: int = _native.QPK_SCATTER_AUTO):
+        """Replace the problem held by this context (qpk_problem_begin again on
+        the same qpk_ctx: buffers, stream and graph state are reused)."""
+        self._upload(problem, bmap, scatter, lambda what: None)
+
+    def _upload(self, problem, bmap, scatter, lap):
         self.n = int(problem.n)
         lin_lower = np.ascontiguousarray(bmap.lin_lower, dtype=np.int64)
         lin_upper = np.ascontiguousarray(bmap.lin_upper, dtype=np.int64)
