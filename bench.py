@@ -646,6 +646,23 @@ def run_ipm(args):
                 "path": "paper_2308_00637_b200.ipm.solve(problem, cfg): upload + solve + x D2H"},
         "gpu_launches": int(launches), "clocks": clk.summary(),
     }
+    if not args.no_cpu_baseline and args.workload != "svm_dual":
+        # the drop-in as a reference user runs it: the reference's OWN IPM loop (host scipy code)
+        # with gpu_direction as its direction_solver (ipm.py:185-212)
+        from oracle import build_ref
+        if build_ref.available():
+            from oracle import refbridge
+            from paper_2308_00637_b200.direction import gpu_direction
+            qp = build_ref.import_qpipm()
+            rcfg = qp.ipm.IpmConfig(gamma=cfg.gamma, mu_init=cfg.mu_init, mu_tol=cfg.mu_tol, mu_shrink=cfg.mu_shrink,
+                                    max_iters=cfg.max_iters,
+                                    pcg=qp.linalg.PcgConfig(tol=cfg.pcg.tol, max_iters=cfg.pcg.max_iters))
+            rrep = qp.ipm.solve(refbridge.ref_problem(problem), rcfg, direction_solver=gpu_direction)
+            line["reference_loop"] = {
+                "value": rrep.wall_time, "unit": "s", "status": rrep.status.value, "ipm_iterations": rrep.iterations,
+                "objective": rrep.objective,
+                "path": "qpipm.ipm.solve(problem, cfg, direction_solver=gpu_direction): the reference's host loop "
+                        "(residuals, rhs, recovery, step in scipy) around the GPU direction solve; upload included"}
     if not args.no_cpu_baseline:
         from oracle import qp_oracle as orc
         k = args.cpu_ipm_iters or (cfg.max_iters if args.workload == "cfg1" else 2)

@@ -386,8 +386,9 @@ __device__ __forceinline__ double hess_sym_t(const Op& op, const double* u, doub
         if (row == lane) ry0 += p[0];
         else if (row == 32 + lane) ry1 += p[0];
       }
-      if (J != cd.x)
-        reinterpret_cast<double2*>(op.H.symp + ((size_t)op.H.nchunks + t) * 64)[lane] = make_double2(cz0, cz1);
+      if (J != cd.x)                                   // column sums of tile (I, J): slot J (J - 1) / 2 + I
+        reinterpret_cast<double2*>(op.H.symp + ((size_t)op.H.nchunks + (size_t)J * (J - 1) / 2 + cd.x) * 64)[lane] =
+            make_double2(cz0, cz1);
     }
     double* rp_ = op.H.symp + (size_t)ch * 64;
     rp_[lane] = ry0;
@@ -409,19 +410,23 @@ __device__ __forceinline__ double sym_combine(const Op& op, const double* u, dou
   const double* colp = op.H.symp + (size_t)op.H.nchunks * 64 + cc;
   double acc = 0.0;
   for (int J = blockIdx.x; J < nt; J += gridDim.x) {
-    const int c0 = __ldg(op.H.rowchunk + J), nrow = __ldg(op.H.rowchunk + J + 1) - c0, items = nrow + J;
-    auto item = [&](int k) -> double {
-      if (k < nrow) return rowp[(size_t)(c0 + k) * 64];
-      const int I = k - nrow;                          // tile (I, J) is tile I nt - I (I - 1) / 2 + (J - I)
-      return colp[((size_t)I * nt - (size_t)I * (I - 1) / 2 + (J - I)) * 64];
-    };
+    // two contiguous runs of 64-double partials: the units of tile row J, then
+    // the tiles (0 .. J-1, J) (stored by tile column: slot J (J - 1) / 2 + I)
+    const int c0 = __ldg(op.H.rowchunk + J), nrow = __ldg(op.H.rowchunk + J + 1) - c0;
+    const double* run[2] = {rowp + (size_t)c0 * 64, colp + (size_t)J * (J - 1) / 2 * 64};
+    const int len[2] = {nrow, J};
     double s = 0.0;
-    int k = part;
-    for (; k + 3 * P < items; k += 4 * P) {
-      const double a0 = item(k), a1 = item(k + P), a2 = item(k + 2 * P), a3 = item(k + 3 * P);
-      s += a0; s += a1; s += a2; s += a3;
+#pragma unroll
+    for (int w = 0; w < 2; ++w) {
+      const double* q = run[w];
+      int k = part;
+      for (; k + 3 * P < len[w]; k += 4 * P) {
+        const double a0 = q[(size_t)k * 64], a1 = q[(size_t)(k + P) * 64], a2 = q[(size_t)(k + 2 * P) * 64],
+                     a3 = q[(size_t)(k + 3 * P) * 64];
+        s += a0; s += a1; s += a2; s += a3;
+      }
+      for (; k < len[w]; k += P) s += q[(size_t)k * 64];
     }
-    for (; k < items; k += P) s += item(k);
     sh[threadIdx.x] = s;
     __syncthreads();
     if (part == 0) {
