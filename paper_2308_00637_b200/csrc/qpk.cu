@@ -2166,7 +2166,6 @@ static Engine make_engine(qpk_ctx* c) {
   E.panel.kp = c->panel_kp; E.panel.ew = c->panel_ew; E.panel.direct = c->panel_direct; E.panel.G = c->panel_grid;
   E.panel.P = c->panel_P.p; E.panel.pcols = c->panel_cols.p; E.panel.eci = c->panel_eci.p; E.panel.ev = c->panel_ev.p;
   E.panel.ppart = c->panel_part.p;
-  E.panel.probe = getenv("QPK_PANEL_PROBE") ? atoi(getenv("QPK_PANEL_PROBE")) : 0;
   const bool pdir = c->scatter == QPK_SCATTER_PANEL && c->panel_direct && c->panel_ew > 0;
   E.panel.cpos = pdir ? c->panel_cpos.p : nullptr;
   E.panel.ue = c->panel_ue.p; E.panel.yrem = c->panel_yrem.p;

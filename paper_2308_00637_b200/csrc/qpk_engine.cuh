@@ -98,7 +98,6 @@ struct Panel {
   int ew;                     // remainder ELL width (0..32)
   int direct;                 // every remainder column has <= 1 entry: y[col] += z a written directly
   int G;                      // CTAs of the panel kernel (partials)
-  int probe;                  // diagnostics only (env QPK_PANEL_PROBE): 1 = consumers skip the math
   const double* P;            // m x kp row-major
   const int* pcols;           // kp panel columns (-1 pads)
   const int* eci;             // m x ew remainder columns (-1 pads)

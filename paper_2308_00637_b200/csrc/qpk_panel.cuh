@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(QPK_PANEL_CW * 32, 1) k_slot_panel(Engine E, i
       const int r0 = ra + it * L.rc, r1 = min(rb, r0 + L.rc);
       const int v0 = r0 & ~1, w0 = (n + r0) & ~1;
       const long long e0 = ((long long)r0 * ew) & ~1LL, c0 = ((long long)r0 * ew) & ~3LL;
-      for (int g0 = warp * RPW; r0 + g0 < r1 && !P.probe; g0 += CW * RPW) {
+      for (int g0 = warp * RPW; r0 + g0 < r1; g0 += CW * RPW) {
         double sum[RPW], ea[RPW];
         double2 av[RPW][Q];                        // the rows, read from shared memory once
 #pragma unroll
