@@ -112,6 +112,9 @@ int qpk_synchronize(qpk_ctx* ctx);
  * qpk_problem_begin with its local sizes. */
 int qpk_nccl_get_unique_id(unsigned char id[128]);
 int qpk_shard_init(qpk_ctx* ctx, int world, int rank, const unsigned char id[128]);
+/* test hook: rank `rank` of `world` without a communicator -- qpk_apply and
+ * qpk_jacobi return this rank's un-reduced share (before qpk_problem_begin) */
+int qpk_shard_emulate(qpk_ctx* ctx, int world, int rank);
 
 /* ---- multi-GPU from ONE process (the reference's solve() is a single
  * process, ipm.py:185-206) ----------------------------------------------------

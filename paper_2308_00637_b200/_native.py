@@ -27,7 +27,7 @@ EXPORTED = (
     "qpk_set_hessian_csr", "qpk_set_hessian_dense", "qpk_set_hessian_lowrank",
     "qpk_problem_finalize", "qpk_set_diagonals", "qpk_set_diagonals_dev", "qpk_jacobi",
     "qpk_apply", "qpk_apply_dev", "qpk_pcg", "qpk_pcg_dev", "qpk_query",
-    "qpk_nccl_get_unique_id", "qpk_shard_init", "qpk_ipm_set_bounds", "qpk_ipm_solve",
+    "qpk_nccl_get_unique_id", "qpk_shard_init", "qpk_shard_emulate", "qpk_ipm_set_bounds", "qpk_ipm_solve",
     "qpk_set_hessian_dense_dev", "qpk_rbf_hessian_dev", "qpk_hessian_apply_dev", "qpk_dense_gemv_dev",
     "qpk_multi_create", "qpk_multi_destroy", "qpk_multi_devices", "qpk_multi_context", "qpk_multi_problem_begin",
     "qpk_multi_problem_add_rows", "qpk_multi_set_hessian_diag", "qpk_multi_set_hessian_csr",
@@ -107,6 +107,7 @@ _SIGS = {
     "qpk_query": ([_P, ctypes.c_char_p], _I64),
     "qpk_nccl_get_unique_id": ([_P], _I),
     "qpk_shard_init": ([_P, _I, _I, _P], _I),
+    "qpk_shard_emulate": ([_P, _I, _I], _I),
     "qpk_ipm_set_bounds": ([_P, _P, _P, _I64, _P, _P, _I64, _P, _P], _I),
     "qpk_ipm_solve": ([_P, ctypes.POINTER(IpmConfig), _P, _P, ctypes.POINTER(IpmResult)], _I),
     "qpk_multi_create": ([_I, ctypes.POINTER(_I), ctypes.POINTER(_P)], _I),

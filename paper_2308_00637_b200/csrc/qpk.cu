@@ -872,6 +872,21 @@ int qpk_shard_init(qpk_ctx* c, int world, int rank, const unsigned char* id) {
   return QPK_OK;
 }
 
+// Test hook: this context behaves as rank `rank` of `world` WITHOUT a
+// communicator -- it holds its row shard, owns its slice of the top block and
+// of the Hessian rows, and qpk_apply / qpk_jacobi return its un-reduced share
+// (the caller sums the shares of all ranks on the host).  Lets one GPU check
+// the partition logic of the N > 1 layout rank by rank, with no kernel of one
+// rank ever waiting on another.
+int qpk_shard_emulate(qpk_ctx* c, int world, int rank) {
+  if (!c || world < 1 || rank < 0 || rank >= world) return fail(QPK_E_ARG, "qpk_shard_emulate: bad arguments");
+  if (c->building || c->finalized) return fail(QPK_E_STATE, "qpk_shard_emulate must precede qpk_problem_begin");
+  c->world = world;
+  c->rank = rank;
+  c->sharded = false;
+  return QPK_OK;
+}
+
 int qpk_problem_begin(qpk_ctx* c, int64_t n, int64_t m_e, int64_t m_l, int64_t m_u) {
   if (!c) return fail(QPK_E_ARG, "null context");
   if (n < 1 || m_e < 0 || m_l < 0 || m_u < 0)

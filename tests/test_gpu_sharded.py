@@ -121,3 +121,94 @@ def test_hook_through_multi_device_layer(monkeypatch):
 def test_multi_device_rejects_duplicate_devices():
     with pytest.raises(_native.NativeUnavailable, match="listed twice"):
         _native.MultiContext([0, 0])
+
+
+# ------------------------------------- N > 1 partition logic, rank by rank --
+class EmulatedRank:
+    """Rank `rank` of `world` without a communicator (qpk_shard_emulate): its row
+    shard of B, its slice of the top block and of the Hessian rows; apply and
+    Jacobi return the rank's un-reduced share.  Ranks run one after the other
+    on the one GPU; the test sums their shares on the host."""
+
+    def __init__(self, problem, bmap, world, rank, scatter):
+        from paper_2308_00637_b200 import sharded
+        from paper_2308_00637_b200.direction import GpuKkt, _csr_arrays
+        self.n = int(problem.n)
+        segs = sharded.b_row_segments(problem, bmap)
+        self.lo, self.hi = sharded.partition_rows(sharded.b_row_nnz(segs), world)[rank]
+        self.ctx = _native.Context(0)
+        self.ctx.call("qpk_shard_emulate", world, rank)
+        self.ctx.call("qpk_problem_begin", self.n, 0, self.hi - self.lo, 0)
+        base = 0
+        for mat, rows, sign in segs:
+            count = mat.n_rows if rows is None else len(rows)
+            a, b = max(self.lo, base), min(self.hi, base + count)
+            if a < b:
+                sel = (np.arange(a - base, b - base, dtype=np.int64) if rows is None
+                       else np.ascontiguousarray(rows[a - base:b - base]))
+                ro, ci, v = _csr_arrays(mat)
+                self.ctx.call("qpk_problem_add_rows", int(mat.n_rows), _native.ptr(ro), _native.ptr(ci),
+                              _native.ptr(v), _native.ptr(sel), len(sel), float(sign))
+            base += count
+        GpuKkt._set_hessian(self, problem.hessian)
+        self.ctx.call("qpk_problem_finalize", int(scatter))
+
+    def share(self, fn, d_diag, q_extra, v=None):
+        d = np.ascontiguousarray(d_diag[self.lo:self.hi])
+        q = np.ascontiguousarray(q_extra, dtype=np.float64)
+        self.ctx.call("qpk_set_diagonals", _native.ptr(d), _native.ptr(q))
+        out = np.empty(self.n + self.hi - self.lo)
+        if fn == "jacobi":
+            self.ctx.call("qpk_jacobi", _native.ptr(out))
+        else:
+            vl = np.ascontiguousarray(np.concatenate([v[:self.n], v[self.n + self.lo:self.n + self.hi]]))
+            self.ctx.call("qpk_apply", _native.ptr(vl), _native.ptr(out))
+        return out
+
+
+EMU = {
+    "rt_tiled_H": (workloads.rt_like, dict(seed=7, n_vox=10000, n_beam=1000, density=0.04), _native.QPK_SCATTER_DICT),
+    "rt_csc": (workloads.rt_like, dict(seed=3, n_vox=6000, n_beam=600, density=0.02), _native.QPK_SCATTER_CSC),
+    "random_diagH": (workloads.random_sweep, dict(seed=5, m=20000, n=5000), _native.QPK_SCATTER_ATOMIC),
+    "svm_panel": (workloads.svm_primal, dict(seed=2, d=40, n_samples=1500), _native.QPK_SCATTER_AUTO),
+}
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("name", sorted(EMU))
+def test_partition_logic_rank_by_rank(name, world):
+    """The N > 1 layout on one GPU, one rank at a time: the ranks' shares of K v
+    (top block: a sum over ranks, what the all-reduce forms; bottom block: the
+    shards side by side) must give the oracle's apply -- every replicated term
+    (diag(Q) u, each Hessian row) is owned by exactly one rank -- and the same
+    for the Jacobi diagonal (diag(H) + q is added by every rank after the
+    reduction, so it is taken out of all shares but one)."""
+    fn, kw, mode = EMU[name]
+    problem, state, meta = fn(**kw)
+    op = build_operator(problem, state)
+    rng = np.random.default_rng(41)
+    v = rng.standard_normal(op.dim)
+    top = np.zeros(op.n)
+    bottom = np.zeros(op.m)
+    jtop = np.zeros(op.n)
+    jbottom = np.zeros(op.m)
+    tiled = 0
+    for rank in range(world):
+        er = EmulatedRank(problem, op.bmap, world, rank, mode)
+        assert er.ctx.query("world") == world and er.ctx.query("rank") == rank
+        tiled += er.ctx.query("hess_tiled")
+        y = er.share("apply", op.d_diag, op.q_diag_extra, v)
+        top += y[:op.n]
+        bottom[er.lo:er.hi] = y[op.n:]
+        j = er.share("jacobi", op.d_diag, op.q_diag_extra)
+        jtop += j[:op.n]
+        jbottom[er.lo:er.hi] = j[op.n:]
+        er.ctx.close()
+    if name == "rt_tiled_H":
+        assert tiled == world                          # every rank tiles its slice of the Hessian rows
+    y_ref = orc.apply_doubly_augmented(op, v)
+    assert parity.rel_err(np.concatenate([top, bottom]), y_ref) <= parity.APPLY_TOL
+    jac_ref = orc.jacobi_diagonal(op)
+    diag_part = orc.hessian_diagonal(problem.hessian) + op.q_diag_extra
+    jtop -= (world - 1) * diag_part
+    assert np.max(np.abs(np.concatenate([jtop, jbottom]) - jac_ref) / np.abs(jac_ref)) <= 1e-11
