@@ -128,6 +128,9 @@ int qpk_shard_emulate(qpk_ctx* ctx, int world, int rank);
 typedef struct qpk_multi qpk_multi;
 int qpk_multi_create(int n_devices, const int* device_ids, qpk_multi** out);
 int qpk_multi_destroy(qpk_multi* mm);
+/* test hook: n_ranks contexts on ONE device with host-mediated all-reduces --
+ * the whole N > 1 sharded engine on a single GPU, no kernel waiting on a peer */
+int qpk_multi_create_emulated(int n_ranks, int device, qpk_multi** out);
 int qpk_multi_devices(qpk_multi* mm);
 qpk_ctx* qpk_multi_context(qpk_multi* mm, int rank);
 int qpk_multi_problem_begin(qpk_multi* mm, int64_t n, int64_t m_e, int64_t m_l, int64_t m_u);

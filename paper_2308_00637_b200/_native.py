@@ -29,7 +29,7 @@ EXPORTED = (
     "qpk_apply", "qpk_apply_dev", "qpk_pcg", "qpk_pcg_dev", "qpk_query",
     "qpk_nccl_get_unique_id", "qpk_shard_init", "qpk_shard_emulate", "qpk_ipm_set_bounds", "qpk_ipm_solve",
     "qpk_set_hessian_dense_dev", "qpk_rbf_hessian_dev", "qpk_hessian_apply_dev", "qpk_dense_gemv_dev",
-    "qpk_multi_create", "qpk_multi_destroy", "qpk_multi_devices", "qpk_multi_context", "qpk_multi_problem_begin",
+    "qpk_multi_create", "qpk_multi_create_emulated", "qpk_multi_destroy", "qpk_multi_devices", "qpk_multi_context", "qpk_multi_problem_begin",
     "qpk_multi_problem_add_rows", "qpk_multi_set_hessian_diag", "qpk_multi_set_hessian_csr",
     "qpk_multi_set_hessian_dense", "qpk_multi_set_hessian_lowrank", "qpk_multi_problem_finalize",
     "qpk_multi_set_diagonals", "qpk_multi_jacobi", "qpk_multi_apply", "qpk_multi_pcg", "qpk_multi_query",
@@ -112,6 +112,7 @@ _SIGS = {
     "qpk_ipm_solve": ([_P, ctypes.POINTER(IpmConfig), _P, _P, ctypes.POINTER(IpmResult)], _I),
     "qpk_multi_create": ([_I, ctypes.POINTER(_I), ctypes.POINTER(_P)], _I),
     "qpk_multi_destroy": ([_P], _I),
+    "qpk_multi_create_emulated": ([_I, _I, ctypes.POINTER(_P)], _I),
     "qpk_multi_devices": ([_P], _I),
     "qpk_multi_context": ([_P, _I], _P),
     "qpk_multi_problem_begin": ([_P, _I64, _I64, _I64, _I64], _I),
@@ -191,11 +192,14 @@ class Context:
 class MultiContext:
     """One libqpk multi-device object (qpk_multi): several GPUs, one process."""
 
-    def __init__(self, devices):
+    def __init__(self, devices, emulate_ranks: int = 0):
         lib = load_library()
         devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices])
         h = ctypes.c_void_p()
-        rc = lib.qpk_multi_create(len(devices), devs, ctypes.byref(h))
+        if emulate_ranks:       # test hook: N ranks on devices[0], host-mediated collectives
+            rc = lib.qpk_multi_create_emulated(int(emulate_ranks), int(devices[0]), ctypes.byref(h))
+        else:
+            rc = lib.qpk_multi_create(len(devices), devs, ctypes.byref(h))
         if rc != QPK_OK:
             raise NativeUnavailable(lib.qpk_last_error().decode(errors="replace"))
         self._lib = lib

@@ -21,6 +21,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -536,6 +538,26 @@ constexpr int NCCL_FLOAT64 = 8, NCCL_SUM = 0;
 
 }  // namespace
 
+// Test-only stand-in for the communicator (qpk_multi_create_emulated): the
+// ranks are contexts of ONE process, each driven by its own host thread; an
+// all-reduce synchronises the rank's stream, meets the other ranks at a host
+// barrier and sums the buffers in rank order on the host.  No kernel ever
+// waits on another rank, so several ranks can share one GPU.
+struct HostComm {
+  int n = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  std::vector<std::vector<double>> bufs;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const long long g = gen;
+    if (++arrived == n) { arrived = 0; ++gen; cv.notify_all(); }
+    else cv.wait(lk, [&] { return gen != g; });
+  }
+};
+
 struct qpk_ctx {
   int device = 0;
   int sms = 0;
@@ -630,6 +652,7 @@ struct qpk_ctx {
   int world = 1, rank = 0;
   bool sharded = false;
   void* comm = nullptr;
+  HostComm* hostcomm = nullptr;   // test-only host-mediated all-reduce (emulated ranks)
   DBuf<double> gscal, lscal2, abuf;
 
   // slot engine
@@ -1874,6 +1897,21 @@ int qpk_set_diagonals_dev(qpk_ctx* c, const double* dd, const double* qq) {
 // in-place sum over ranks on the context's stream (sharded mode only)
 static int allreduce_sum(qpk_ctx* c, double* buf, size_t count, cudaStream_t s) {
   if (!c->sharded || count == 0) return QPK_OK;
+  if (c->hostcomm) {
+    HostComm* hc = c->hostcomm;
+    std::vector<double>& mine = hc->bufs[c->rank];
+    mine.resize(count);
+    CUDA_TRY(cudaMemcpyAsync(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    hc->barrier();
+    std::vector<double> sum(count, 0.0);
+    for (int r = 0; r < hc->n; ++r)
+      for (size_t i = 0; i < count; ++i) sum[i] += hc->bufs[r][i];
+    hc->barrier();                                   // every rank has read all buffers
+    CUDA_TRY(cudaMemcpyAsync(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return QPK_OK;
+  }
   const int rc = nccl().allReduce(buf, buf, count, NCCL_FLOAT64, NCCL_SUM, c->comm, s);
   if (rc != 0) return fail(QPK_E_CUDA, "ncclAllReduce failed: %s", nccl().errStr ? nccl().errStr(rc) : "?");
   return QPK_OK;
@@ -2138,10 +2176,10 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   // r'r and r'z, and the control decision.
   if (csc) k_shard_reduce<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
   else k_shard_reduce<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
-  nccl().groupStart();
+  if (!c->hostcomm) nccl().groupStart();
   allreduce_sum(c, c->y.p, c->n, s);
   allreduce_sum(c, c->gscal.p, 4, s);
-  nccl().groupEnd();
+  if (!c->hostcomm) nccl().groupEnd();
   k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
   allreduce_sum(c, c->lscal2.p, 2, s);
   k_slot_decide<<<1, 32, 0, s>>>(E, par);
@@ -2246,7 +2284,7 @@ static int engine_setup(qpk_ctx* c) {
 static int engine_graph(qpk_ctx* c, int slots) {
   if (c->graph && c->graph_slots == slots) return QPK_OK;
   if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
-  if (c->graph_failed) return QPK_OK;
+  if (c->graph_failed || c->hostcomm) return QPK_OK;   // (host-mediated collectives cannot be captured)
   Engine E = make_engine(c);
   cudaStream_t cs = c->own;
   cudaGraph_t g = nullptr;

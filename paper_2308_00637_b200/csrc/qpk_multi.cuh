@@ -10,6 +10,7 @@ struct qpk_multi {
   std::vector<int> devs;
   std::vector<qpk_ctx*> ctx;
   bool comm_ready = false;
+  HostComm* hostcomm = nullptr;         // emulated ranks (test only): host-mediated all-reduce
   // problem being described (the caller's arrays stay valid until finalize)
   struct Seg { int64_t n_rows; const int64_t* ro; const int64_t* ci; const double* v; std::vector<int64_t> rows; double sign; };
   std::vector<Seg> segs;
@@ -76,7 +77,35 @@ int qpk_multi_create(int n_devices, const int* device_ids, qpk_multi** out) {
 int qpk_multi_destroy(qpk_multi* mm) {
   if (!mm) return QPK_OK;
   for (qpk_ctx* c : mm->ctx) qpk_destroy(c);
+  delete mm->hostcomm;
   delete mm;
+  return QPK_OK;
+}
+
+// Test hook: `n_ranks` contexts on ONE device, their collectives mediated by
+// the host (HostComm).  The whole N > 1 sharded engine -- row shards, slices
+// of the top block and of the Hessian rows, every all-reduce of a slot, the
+// decision kernel -- runs on a single GPU, rank kernels never waiting on one
+// another.
+int qpk_multi_create_emulated(int n_ranks, int device, qpk_multi** out) {
+  if (!out || n_ranks < 1) return fail(QPK_E_ARG, "qpk_multi_create_emulated: bad arguments");
+  qpk_multi* mm = new qpk_multi();
+  for (int r = 0; r < n_ranks; ++r) {
+    qpk_ctx* c = nullptr;
+    const int rc = qpk_create(device, &c);
+    if (rc != QPK_OK) {
+      for (qpk_ctx* p : mm->ctx) qpk_destroy(p);
+      delete mm;
+      return rc;
+    }
+    mm->devs.push_back(device);
+    mm->ctx.push_back(c);
+  }
+  mm->buf.resize(n_ranks);
+  mm->hostcomm = new HostComm();
+  mm->hostcomm->n = n_ranks;
+  mm->hostcomm->bufs.resize(n_ranks);
+  *out = mm;
   return QPK_OK;
 }
 
@@ -155,15 +184,19 @@ int qpk_multi_problem_finalize(qpk_multi* mm, int scatter) {
   mm->hi[nd - 1] = mm->m;
   // one communicator per device, created from the device threads with one id
   unsigned char id[128];
-  if (!mm->comm_ready) {
+  if (!mm->comm_ready && !mm->hostcomm) {
     int rc = qpk_nccl_get_unique_id(id);
     if (rc != QPK_OK) return rc;
   }
   int rc = multi_run(mm, [&](int r) -> int {
     qpk_ctx* c = mm->ctx[r];
     if (!mm->comm_ready) {
-      int e = qpk_shard_init(c, nd, r, id);
-      if (e != QPK_OK) return e;
+      if (mm->hostcomm) {                              // emulated ranks: no NCCL
+        c->world = nd; c->rank = r; c->sharded = true; c->hostcomm = mm->hostcomm;
+      } else {
+        int e = qpk_shard_init(c, nd, r, id);
+        if (e != QPK_OK) return e;
+      }
     }
     int e = qpk_problem_begin(c, mm->n, 0, mm->hi[r] - mm->lo[r], 0);
     if (e != QPK_OK) return e;

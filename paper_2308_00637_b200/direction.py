@@ -156,8 +156,8 @@ class MultiGpuKkt(GpuKkt):
     (ipm.py:185-206) can use N GPUs through the unmodified hook.  Same methods
     and global-sized vectors as GpuKkt."""
 
-    def __init__(self, problem, bmap, devices, scatter: int = _native.QPK_SCATTER_AUTO):
-        self.ctx = _native.MultiContext(devices)
+    def __init__(self, problem, bmap, devices, scatter: int = _native.QPK_SCATTER_AUTO, emulate_ranks: int = 0):
+        self.ctx = _native.MultiContext(devices, emulate_ranks=emulate_ranks)
         self.devices = list(devices)
         self.n = int(problem.n)
         lin_lower = np.ascontiguousarray(bmap.lin_lower, dtype=np.int64)

@@ -147,3 +147,32 @@ def test_restart_branch(mode, monkeypatch):
         print(f"mode {mode} engine {engine}: {info.iterations} iterations, {info.restarts} restarts "
               f"(oracle {ref.iterations}, {ref_restarts})")
         gk.close()
+
+
+@pytest.mark.slow
+def test_full_scale_cfg3_eight_emulated_ranks():
+    """cfg3 at full size through the N = 8 sharded engine on one GPU
+    (qpk_multi_create_emulated: host-mediated collectives, no kernel waits on a
+    peer): every rank tiles its row shard and its slice of the Hessian rows;
+    apply, Jacobi and the first 20 residuals against the oracle."""
+    from paper_2308_00637_b200.direction import MultiGpuKkt
+    problem, state, meta = workloads.rt_like(seed=3)
+    op = build_operator(problem, state)
+    mk = MultiGpuKkt(problem, op.bmap, devices=[0], emulate_ranks=8)
+    assert all(mk.ctx.query("scatter", r) == _native.QPK_SCATTER_DICT and mk.ctx.query("hess_tiled", r) == 1
+               for r in range(8))
+    mk.set_diagonals(op.d_diag, op.q_diag_extra)
+    rng = np.random.default_rng(77)
+    jac, ref_jac = mk.jacobi(), orc.jacobi_diagonal(op)
+    assert np.max(np.abs(jac - ref_jac) / np.abs(ref_jac)) <= parity.APPLY_TOL
+    v = rng.standard_normal(op.dim)
+    assert parity.rel_err(mk.apply(v), orc.apply_doubly_augmented(op, v)) <= parity.APPLY_TOL
+    rhs = rng.standard_normal(op.dim)
+    cfg = orc.PcgConfig(tol=1e-300, max_iters=20)
+    ref, ref_hist = oracle_history(op, rhs, cfg)
+    x, info, hist = mk.pcg(rhs, cfg.tol, cfg.max_iters, True, history=True)
+    assert info.iterations == 20
+    dev = np.max(np.abs(hist - ref_hist) / ref_hist)
+    assert dev <= parity.HIST_TOL, dev
+    assert parity.rel_err(x, ref.solution) <= 1e-8
+    mk.close()

@@ -212,3 +212,37 @@ def test_partition_logic_rank_by_rank(name, world):
     diag_part = orc.hessian_diagonal(problem.hessian) + op.q_diag_extra
     jtop -= (world - 1) * diag_part
     assert np.max(np.abs(np.concatenate([jtop, jbottom]) - jac_ref) / np.abs(jac_ref)) <= 1e-11
+
+
+@pytest.mark.parametrize("ranks", [2, 3])
+@pytest.mark.parametrize("mode", [_native.QPK_SCATTER_AUTO, _native.QPK_SCATTER_CSC, _native.QPK_SCATTER_DICT])
+@pytest.mark.parametrize("name", sorted(SPECS))
+def test_sharded_engine_with_emulated_ranks(name, mode, ranks):
+    """The WHOLE N > 1 sharded engine on one GPU (qpk_multi_create_emulated):
+    N contexts on device 0, each with its row shard, its slice of the top
+    block and of the Hessian rows, driven by N host threads; the slot's
+    collectives ([y_top | 4 scalars], [r'r, r'z], ||rhs||^2, the Jacobi
+    partial) are mediated by the host (stream sync, barrier, sum in rank
+    order), so no kernel of one rank waits on another.  Same gates as the
+    single-GPU parity tests."""
+    from paper_2308_00637_b200.direction import MultiGpuKkt
+    fn, kw = SPECS[name]
+    problem, state, meta = fn(**kw)
+    op = build_operator(problem, state)
+    pre = name + "_"
+    mk = MultiGpuKkt(problem, op.bmap, devices=[0], scatter=mode, emulate_ranks=ranks)
+    assert mk.ctx.query("world") == ranks and mk.ctx.query("rank", ranks - 1) == ranks - 1
+    bounds = [(mk.ctx.query("row_lo", r), mk.ctx.query("row_hi", r)) for r in range(ranks)]
+    assert bounds[0][0] == 0 and bounds[-1][1] == op.m and all(a[1] == b[0] for a, b in zip(bounds, bounds[1:]))
+    mk.set_diagonals(op.d_diag, op.q_diag_extra)
+    assert parity.rel_err(mk.jacobi(), CFG[pre + "jacobi"]) <= parity.APPLY_TOL
+    for v, y in zip(CFG[pre + "vecs"], CFG[pre + "applies"]):
+        assert parity.rel_err(mk.apply(v), y) <= parity.APPLY_TOL
+    rhs = CFG[pre + "rhs"]
+    cfg = orc.PcgConfig(tol=1e-300, max_iters=200) if name == "cfg5" else orc.PcgConfig(tol=1e-7, max_iters=400)
+    x, info, hist = mk.pcg(rhs, cfg.tol, cfg.max_iters, True, history=True)
+    ok, msg = parity.check_history(hist, CFG[pre + "pcg_hist"], parity.envelope(op, rhs, cfg, CFG[pre + "pcg_hist"]))
+    assert ok, msg
+    if int(CFG[pre + "pcg_conv"]):
+        assert info.converged and parity.rel_err(x, CFG[pre + "pcg_x"]) <= 1e-5
+    mk.close()
