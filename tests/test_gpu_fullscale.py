@@ -150,7 +150,8 @@ def test_restart_branch(mode, monkeypatch):
 
 
 @pytest.mark.slow
-def test_full_scale_cfg3_eight_emulated_ranks():
+@pytest.mark.parametrize("mode", [_native.QPK_SCATTER_AUTO, _native.QPK_SCATTER_DICT])
+def test_full_scale_cfg3_eight_emulated_ranks(mode):
     """cfg3 at full size through the N = 8 sharded engine on one GPU
     (qpk_multi_create_emulated: host-mediated collectives, no kernel waits on a
     peer): every rank tiles its row shard and its slice of the Hessian rows;
@@ -158,9 +159,12 @@ def test_full_scale_cfg3_eight_emulated_ranks():
     from paper_2308_00637_b200.direction import MultiGpuKkt
     problem, state, meta = workloads.rt_like(seed=3)
     op = build_operator(problem, state)
-    mk = MultiGpuKkt(problem, op.bmap, devices=[0], emulate_ranks=8)
-    assert all(mk.ctx.query("scatter", r) == _native.QPK_SCATTER_DICT and mk.ctx.query("hess_tiled", r) == 1
-               for r in range(8))
+    mk = MultiGpuKkt(problem, op.bmap, devices=[0], scatter=mode, emulate_ranks=8)
+    fmt = [(mk.ctx.query("scatter", r), mk.ctx.query("hess_tiled", r)) for r in range(8)]
+    print("per-rank (format, Hessian tiles):", fmt)
+    # (AUTO decides per rank: a 1/8 shard of cfg3 is below the tile format's size threshold -> CSC)
+    if mode == _native.QPK_SCATTER_DICT:
+        assert all(f == (_native.QPK_SCATTER_DICT, 1) for f in fmt)
     mk.set_diagonals(op.d_diag, op.q_diag_extra)
     rng = np.random.default_rng(77)
     jac, ref_jac = mk.jacobi(), orc.jacobi_diagonal(op)
