@@ -2084,7 +2084,7 @@ static bool comb_direct(const qpk_ctx* c) { return c->scatter == QPK_SCATTER_DIC
 // update kernel (top_value<3>, same order as k_comb_direct), one launch less
 static bool comb_fused(const qpk_ctx* c) {
   static const int env = getenv("QPK_FUSE_COMB") ? atoi(getenv("QPK_FUSE_COMB")) : 1;
-  return env != 0 && comb_direct(c) && !c->sharded;
+  return env != 0 && comb_direct(c);      // (sharded: summed inside k_shard_reduce<3> instead)
 }
 
 // does the slot finish B'z with a CSC gather pass (k_slot_csc + seg sums)?
@@ -2175,6 +2175,7 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   // of [y_top | scalars], the update on the now-global y, an all-reduce of
   // r'r and r'z, and the control decision.
   if (csc) k_shard_reduce<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  else if (comb_fused(c)) k_shard_reduce<3><<<G, QPK_BLOCK, 0, s>>>(E, par);   // + the CTA-partial combine
   else k_shard_reduce<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
   if (!c->hostcomm) nccl().groupStart();
   allreduce_sum(c, c->y.p, c->n, s);
