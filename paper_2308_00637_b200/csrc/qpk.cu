@@ -1805,7 +1805,6 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   c->h_nchunks = 0;
   if (c->hkind == QPK_HESS_DENSE && c->cl_C == 0 && !c->sharded && c->n >= QPK_SYM_MIN_N && !getenv("QPK_NO_SYM")) {
     const int nt = (int)((c->n + 63) / 64);
-    const size_t tiles = (size_t)nt * (nt + 1) / 2;
     // only a bitwise symmetric H may be packed; any other DenseHessian keeps
     // the row-major apply (h.m @ v for whatever m is, as the reference)
     DBuf<int> bad;
@@ -2072,7 +2071,7 @@ static void launch_slot_rows_t(const qpk_ctx* c, int grid, cudaStream_t s, const
 
 // PDL on the tile / panel slot chains (top -> pass over B -> combine -> update)
 static bool slot_pdl(const qpk_ctx* c) {
-  static const int env = getenv("QPK_PDL") ? atoi(getenv("QPK_PDL")) : 1;
+  const int env = getenv("QPK_PDL") ? atoi(getenv("QPK_PDL")) : 1;
   return env != 0 && !c->sharded &&
          (c->scatter == QPK_SCATTER_DICT || (c->scatter == QPK_SCATTER_PANEL && c->panel_direct));
 }
@@ -2083,8 +2082,16 @@ static bool comb_direct(const qpk_ctx* c) { return c->scatter == QPK_SCATTER_DIC
 // tile mode, single-level combine: the CTA partials are summed inside the
 // update kernel (top_value<3>, same order as k_comb_direct), one launch less
 static bool comb_fused(const qpk_ctx* c) {
-  static const int env = getenv("QPK_FUSE_COMB") ? atoi(getenv("QPK_FUSE_COMB")) : 1;
+  const int env = getenv("QPK_FUSE_COMB") ? atoi(getenv("QPK_FUSE_COMB")) : 1;
   return env != 0 && comb_direct(c);      // (sharded: summed inside k_shard_reduce<3> instead)
+}
+
+// sharded tile format: the residual scalars [r'r, r'z] ride in the slot's one
+// all-reduce (k_slot_update has the algebra); QPK_SHARD_FOLD=0 keeps the
+// second all-reduce + decision kernel
+static bool slot_fold(const qpk_ctx* c) {
+  const int env = getenv("QPK_SHARD_FOLD") ? atoi(getenv("QPK_SHARD_FOLD")) : 1;
+  return env != 0 && c->sharded && c->scatter == QPK_SCATTER_DICT && c->cacc;
 }
 
 // does the slot finish B'z with a CSC gather pass (k_slot_csc + seg sums)?
@@ -2100,7 +2107,7 @@ static int slot_launches(const qpk_ctx* c) {
   else if (c->scatter == QPK_SCATTER_PANEL)
     k += 2 + (c->hkind != QPK_HESS_DIAG ? 1 : 0) + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 1 : 0);
   else k += 1 + (slot_csc(c) ? 1 : 0) + (c->h_nchunks ? 2 : 0) + (c->n_dense ? 1 : 0);
-  if (c->sharded) k += 2;
+  if (c->sharded) k += slot_fold(c) ? 1 : 2;
   return k;
 }
 
@@ -2177,11 +2184,13 @@ static void launch_slot(qpk_ctx* c, const Engine& E, int par, cudaStream_t s) {
   if (csc) k_shard_reduce<2><<<G, QPK_BLOCK, 0, s>>>(E, par);
   else if (comb_fused(c)) k_shard_reduce<3><<<G, QPK_BLOCK, 0, s>>>(E, par);   // + the CTA-partial combine
   else k_shard_reduce<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  const bool fold = slot_fold(c);
   if (!c->hostcomm) nccl().groupStart();
   allreduce_sum(c, c->y.p, c->n, s);
-  allreduce_sum(c, c->gscal.p, 4, s);
+  allreduce_sum(c, c->gscal.p, fold ? 10 : 4, s);
   if (!c->hostcomm) nccl().groupEnd();
   k_slot_update<1><<<G, QPK_BLOCK, 0, s>>>(E, par);
+  if (fold) return;                                  // the update kernel's last block decided
   allreduce_sum(c, c->lscal2.p, 2, s);
   k_slot_decide<<<1, 32, 0, s>>>(E, par);
 }
@@ -2228,6 +2237,7 @@ static Engine make_engine(qpk_ctx* c) {
   E.n_seg = c->n_seg; E.seg_lanes = c->seg_lanes;
   E.scatter = c->scatter;
   E.sharded = c->sharded ? 1 : 0;
+  E.fold = slot_fold(c) ? 1 : 0;
   if (c->n_dense && (c->scatter == QPK_SCATTER_ATOMIC || c->scatter == QPK_SCATTER_CSC)) {
     E.op.r0 = c->n_dense; E.op.ndense = c->n_dense; E.op.cdense = c->cdense.p;
   }
@@ -2269,7 +2279,7 @@ static int engine_setup(qpk_ctx* c) {
   }
   if (c->ctrl.p) return QPK_OK;
   CUDA_TRY(c->ctrl.alloc(2));
-  CUDA_TRY(c->gscal.alloc(4));
+  CUDA_TRY(c->gscal.alloc(10));
   CUDA_TRY(c->lscal2.alloc(2));
   CUDA_TRY(c->abuf.alloc(2));
   CUDA_TRY(c->counter.alloc(1));

@@ -313,7 +313,6 @@ __global__ void __launch_bounds__(QPK_CL_THREADS, 1) k_pcg_cluster(ClParams P) {
   if (rnorm <= thr) { conv = 1; done = true; }                      // linalg.py:93-94
   bool restart = true;
   double rz = 0.0, beta = 0.0;
-  bool have_best_x = true;                                          // best = x0 = 0 initially
   for (long long k = 1; !done && k <= P.max_iters; ++k) {
     // ---- direction: z = M^-1 r, p = z (+ beta p); top replicated, bottom owned
     double rzt = 0.0, rzb = 0.0;
@@ -379,7 +378,6 @@ __global__ void __launch_bounds__(QPK_CL_THREADS, 1) k_pcg_cluster(ClParams P) {
       best_rnorm = rnorm;
       for (int j = threadIdx.x; j < n; j += blockDim.x) sm[L.xb_t + j] = sm[L.x_t + j];
       for (int i = threadIdx.x; i < mr; i += blockDim.x) sm[L.xb_b + i] = sm[L.x_b + i];
-      have_best_x = false;                                          // best is a later iterate now
     }
     if (rnorm <= thr) {                                             // linalg.py:112-125
       __syncthreads();
@@ -402,7 +400,6 @@ __global__ void __launch_bounds__(QPK_CL_THREADS, 1) k_pcg_cluster(ClParams P) {
     restart = false;
     __syncthreads();
   }
-  (void)have_best_x;
   // result buffer: 0 = x (converged), 1 = best iterate (cap / breakdown)
   int result = 0;
   if (!done) {

@@ -65,7 +65,9 @@ struct Op {
 // partial-sum slots (slot-major: part[slot * G + cta])
 #define QPK_DENSE_ROWS_MAX 4
 enum { SLOT_ROWS = 0, SLOT_PREP = 1, SLOT_RR = 2, SLOT_RZ = 3, SLOT_AUX = 4, SLOT_AUX2 = 5, SLOT_S = 6,
-       SLOT_DR = SLOT_S + QPK_KMAX, NSLOTS = SLOT_DR + QPK_DENSE_ROWS_MAX };
+       SLOT_DR = SLOT_S + QPK_KMAX, SLOT_F = SLOT_DR + QPK_DENSE_ROWS_MAX, NSLOTS = SLOT_F + 6 };
+// SLOT_F .. SLOT_F+5 (sharded tile format, one all-reduce per iteration): this rank's bottom-block
+// sums  sum r^2, sum r y, sum y^2  and the same weighted by M^-1 = 1/d -- see k_slot_update
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;

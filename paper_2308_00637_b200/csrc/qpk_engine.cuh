@@ -117,6 +117,7 @@ struct Engine {
   Panel panel;
   int scatter;                // 1 atomic, 2 CSC segments, 3 row-block dictionary, 4 dense panel
   int sharded;                // row-sharded over ranks: collectives between the slot kernels
+  int fold;                   // sharded tile format: [r'r, r'z] folded into the slot's one all-reduce
   double* gscal;              // [4] rank-summed ROWS, PREP, AUX, AUX2 totals (sharded)
   double* lscal2;             // [2] r'r, r'z (rank-local, then rank-summed)
   double* abuf;               // [2] alpha and the r'z it used (identical on every rank)
@@ -416,19 +417,27 @@ __device__ __forceinline__ double top_value(const Engine& E, int j) {
 // then summed over ranks by one grouped all-reduce.
 template <int SC>
 __global__ void __launch_bounds__(QPK_BLOCK) k_shard_reduce(Engine E, int par) {
-  __shared__ double red[32];
   const Ctrl c = E.ctrl[par];
   if (c.mode == MODE_DONE) return;
   if (SC != 1)
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < E.op.n; j += gridDim.x * blockDim.x)
       E.y[j] = top_value<SC>(E, j);
   if (!last_block(E.counter)) return;
+  // the last block: one warp per scalar, all of them side by side (lane-strided
+  // partial sums, then a butterfly: a fixed order)
   const int G = E.G;
-  const double t0 = grid_total(E.part + SLOT_ROWS * G, E.G_rows, red);
-  const double t1 = grid_total(E.part + SLOT_PREP * G, G, red);
-  const double t2 = grid_total(E.part + SLOT_AUX * G, G, red);
-  const double t3 = grid_total(E.part + SLOT_AUX2 * G, E.G_rows, red);
-  if (threadIdx.x == 0) { E.gscal[0] = t0; E.gscal[1] = t1; E.gscal[2] = t2; E.gscal[3] = t3; }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int nq = E.fold ? 10 : 4;
+  for (int q = warp; q < nq; q += nw) {
+    const int slot = q == 0 ? SLOT_ROWS : q == 1 ? SLOT_PREP : q == 2 ? SLOT_AUX : q == 3 ? SLOT_AUX2 : SLOT_F + (q - 4);
+    const int cnt = (q == 1 || q == 2) ? G : E.G_rows;
+    const double* src = E.part + slot * G;
+    double t = 0.0;
+    for (int i = lane; i < cnt; i += 32) t += src[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) E.gscal[q] = t;
+  }
 }
 
 
@@ -553,7 +562,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
       const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
       E.r[i] = ri;
-      if (owns(op, i)) {
+      if (E.fold ? i < op.n : owns(op, i)) {
         rr += ri * ri;
         rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
       }
@@ -584,7 +593,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
             ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yv[u].y));
             r2[i] = ri;
             // replicated top entries count once over the ranks (rank 0)
-            const bool cx = owns(op, 2 * i), cy = owns(op, 2 * i + 1);
+            const bool cx = E.fold ? 2 * i < op.n : owns(op, 2 * i), cy = E.fold ? 2 * i + 1 < op.n : owns(op, 2 * i + 1);
             if (cx) { rr += ri.x * ri.x; rzn += ri.x * __dmul_rn(mv[u].x, ri.x); }
             if (cy) { rr += ri.y * ri.y; rzn += ri.y * __dmul_rn(mv[u].y, ri.y); }
           }
@@ -593,7 +602,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       if ((N & 1) && N - 1 >= nb && blockIdx.x == 0 && threadIdx.x == 0) {
         const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
         E.r[N - 1] = ri;
-        if (owns(op, N - 1)) {
+        if (E.fold ? N - 1 < op.n : owns(op, N - 1)) {
           rr += ri * ri;
           rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
         }
@@ -606,7 +615,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       const double yi = (CSC && i < op.n) ? top_value<SC>(E, i) : E.y[i];
       const double ri = __dsub_rn(__ldg(E.rhs + i), yi);
       if (store) E.r[i] = ri;
-      if (owns(op, i)) rr += ri * ri;
+      if (E.fold ? i < op.n : owns(op, i)) rr += ri * ri;
     }
   }
   double t = block_sum(rr, red);
@@ -619,6 +628,23 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
   double rr_tot, rz_tot;
   grid_total2(E.part + SLOT_RR * G, G, E.part + SLOT_RZ * G, G, red, rr_tot, rz_tot);
   if (threadIdx.x != 0) return;
+  if (E.fold) {
+    // One all-reduce per iteration: every rank summed the WHOLE replicated top
+    // block above (identical on all ranks); the bottom block's share comes
+    // from the sums the tile pass formed before alpha was known and the slot's
+    // all-reduce added over the ranks:
+    //   |r - a y|^2 = r'r - 2 a r'y + a^2 y'y      (and the same weighted by M^-1)
+    // (explicit-residual slots: gscal[4] = sum (rhs - y)^2 over the bottom block)
+    const double* F = E.gscal + 4;
+    if (c.mode == MODE_NORMAL || c.mode == MODE_RESTART) {
+      rr_tot += fma(alpha, fma(alpha, F[2], -2.0 * F[1]), F[0]);
+      rz_tot += fma(alpha, fma(alpha, F[5], -2.0 * F[4]), F[3]);
+    } else {
+      rr_tot += F[0];
+    }
+    decide(E, c, par, rr_tot, rz_tot, alpha, rz, t_upd);
+    return;
+  }
   if (E.sharded) {
     // rank-local totals; summed over ranks by the collective, then k_slot_decide
     E.lscal2[0] = rr_tot;

@@ -96,7 +96,7 @@ __global__ void k_ipm_qextra_hi(IpmDev P, double* q) {
 __global__ void __launch_bounds__(QPK_BLOCK) k_ipm_residuals(IpmDev P, double mu) {
   __shared__ double red[32];
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
-  double pr = 0.0, du = 0.0, co = 0.0, re = 0.0, bad = 0.0;
+  double pr = 0.0, co = 0.0, re = 0.0, bad = 0.0;
   for (int j = tid; j < P.n; j += nth) {
     const double v = (P.hx[j] + P.pvec[j]) - P.btl[j];
     P.rH[j] = v;

@@ -153,6 +153,7 @@ k_slot_rows_tile(Engine E, int par) {
     cacc[(i / nu) * QPK_TILE_UMAX + (i % nu)] = 0.0;
   __syncthreads();
   double pacc = 0.0, rzb = 0.0;
+  double fs[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};     // folded bottom sums (E.fold)
   if (warp == CW) {
     // ---------------------------------------------------------- producer ----
     // In a PCG iteration (fuse) it streams only data written two or more
@@ -381,6 +382,16 @@ k_slot_rows_tile(Engine E, int par) {
         E.y[op.n + r] = yb;
         pacc += tt * z + wr * yb;
         S.zs[g][rr] = z;
+        if (E.fold) {
+          if (fuse) {
+            const double rres = st.r[op.n + r - st.w0], mi = 1.0 / dr;
+            fs[0] += rres * rres; fs[1] += rres * yb; fs[2] += yb * yb;
+            fs[3] += rres * __dmul_rn(mi, rres); fs[4] += rres * __dmul_rn(mi, yb); fs[5] += yb * __dmul_rn(mi, yb);
+          } else {
+            const double e = __dsub_rn(__ldg(E.rhs + op.n + r), yb);   // explicit residual (the update kernel stores it)
+            fs[0] += e * e;
+          }
+        }
       }
       tile_group_bar(g);
       for (int cc = tid; cc < nd; cc += T) {
@@ -431,6 +442,13 @@ k_slot_rows_tile(Engine E, int par) {
   if (threadIdx.x == 0) E.part[SLOT_ROWS * E.G + blockIdx.x] = t;
   t = block_sum(rzb, S.red);
   if (threadIdx.x == 0) E.part[SLOT_AUX2 * E.G + blockIdx.x] = t;
+  if (E.fold) {
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      t = block_sum(fs[q], S.red);
+      if (threadIdx.x == 0) E.part[(SLOT_F + q) * E.G + blockIdx.x] = t;
+    }
+  }
 }
 
 // y_top += H' u for CSR / dense / low-rank H, its u'H'u added to the slot's

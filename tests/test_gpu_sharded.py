@@ -214,6 +214,33 @@ def test_partition_logic_rank_by_rank(name, world):
     assert np.max(np.abs(np.concatenate([jtop, jbottom]) - jac_ref) / np.abs(jac_ref)) <= 1e-11
 
 
+@pytest.mark.parametrize("fold", ["1", "0"])
+def test_sharded_tile_slot_with_and_without_folded_scalars(monkeypatch, fold):
+    """Sharded tile format: [r'r, r'z] ride in the slot's one all-reduce (default;
+    the bottom block's share through |r - a y|^2 = r'r - 2a r'y + a^2 y'y), or
+    take the second all-reduce + decision kernel (QPK_SHARD_FOLD=0).  Both must
+    hold the literal 1e-8 on the first 60 residuals of an RT-like system at 3
+    emulated ranks, and agree on the solution."""
+    from paper_2308_00637_b200.direction import MultiGpuKkt
+    monkeypatch.setenv("QPK_SHARD_FOLD", fold)
+    problem, state, meta = workloads.rt_like(seed=7, n_vox=20000, n_beam=2000, density=0.02)
+    op = build_operator(problem, state)
+    rhs = np.random.default_rng(5).standard_normal(op.dim)
+    cfg = orc.PcgConfig(tol=1e-300, max_iters=60)
+    ref_hist = []
+    ref = orc.pcg_direction(op, rhs, cfg, callback=lambda k, xk, rn: ref_hist.append(rn))
+    ref_hist = np.array([np.linalg.norm(rhs)] + ref_hist)
+    mk = MultiGpuKkt(problem, op.bmap, devices=[0], scatter=_native.QPK_SCATTER_DICT, emulate_ranks=3)
+    mk.set_diagonals(op.d_diag, op.q_diag_extra)
+    x, info, hist = mk.pcg(rhs, cfg.tol, cfg.max_iters, True, history=True)
+    launches = mk.ctx.query("kernel_launches")
+    mk.close()
+    ok, msg = parity.check_history(hist, ref_hist, parity.envelope(op, rhs, cfg, ref_hist))
+    assert ok, msg
+    assert parity.rel_err(x, ref.solution) <= 1e-6
+    print(f"fold={fold}: max history deviation {np.max(np.abs(hist - ref_hist) / ref_hist):.2e}, launches {launches}")
+
+
 @pytest.mark.parametrize("ranks", [2, 3])
 @pytest.mark.parametrize("mode", [_native.QPK_SCATTER_AUTO, _native.QPK_SCATTER_CSC, _native.QPK_SCATTER_DICT])
 @pytest.mark.parametrize("name", sorted(SPECS))
