@@ -105,9 +105,11 @@ int qpk_synchronize(qpk_ctx* ctx);
 
 /* ---- multi-GPU: row sharding of B over ranks (one process per GPU) ------
  * Rank r holds rows [lo_r, hi_r) of B and the matching slice of every bottom
- * vector; the top block (n) is replicated.  Per PCG iteration the ranks
- * all-reduce [y_top partial | 4 scalars] and [r'r, r'z] with NCCL (SURVEY.md
- * 8(e)).  Rank 0 obtains the id, the launcher broadcasts it (e.g. through
+ * vector; the top block (n) is replicated, every rank owning a slice of its
+ * terms.  Per PCG iteration the ranks all-reduce [y_top partial | slot scalars]
+ * with NCCL; the tile format folds [r'r, r'z] into that one
+ * all-reduce, the other formats reduce them in a second, 2-value all-reduce.
+ * Rank 0 obtains the id, the launcher broadcasts it (e.g. through
  * torch.distributed), every rank calls qpk_shard_init before
  * qpk_problem_begin with its local sizes. */
 int qpk_nccl_get_unique_id(unsigned char id[128]);

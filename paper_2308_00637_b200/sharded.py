@@ -2,10 +2,12 @@
 
 B = (C; A_l; -A_u) is split into contiguous, nnz-balanced row blocks, one per
 rank; every bottom vector (w, D, r, p, x, ...) is split the
-same way and the top block (n) is replicated.  Inside the library each PCG
-iteration all-reduces [y_top partial | 4 scalars] and [r'r, r'z] over NCCL on
-the solver's own stream (`qpk_shard_init`); torch.distributed is only the
-plumbing that broadcasts the NCCL id and gathers the solution.
+same way and the top block (n) is replicated, every rank owning a slice of
+its terms.  Inside the library each PCG iteration all-reduces
+[y_top partial | slot scalars] over NCCL on the solver's own stream
+(`qpk_shard_init`) -- in the tile format that one all-reduce also carries
+[r'r, r'z]; torch.distributed is only the plumbing that broadcasts the NCCL id
+and gathers the solution.
 
 `ShardedKkt` mirrors `direction.GpuKkt` with global-sized inputs and outputs,
 so `sharded_direction(op, rhs, cfg)` is a drop-in `DirectionSolver` for an
