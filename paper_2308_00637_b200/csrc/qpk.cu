@@ -1379,14 +1379,38 @@ static int build_dict(qpk_ctx* c, bool probe) {
     // test switch: fewer CTAs -> long per-CTA tile streams on small problems
     // (ring-stage reuse, descriptor refill, L2 prefetch; tests/test_gpu_fullscale.py)
     if (const char* ev = getenv("QPK_TILE_GRID")) G = std::max(1, std::min(G, atoi(ev)));
-    std::vector<long long> pre(tid + 1, 0);
     // weight = dense slots + a fixed per-tile cost (barriers, copies) of ~2k slots
-    for (int t = 0; t < tid; ++t) pre[t + 1] = pre[t] + (long long)(tiles[t].rb - tiles[t].ra) * tiles[t].pad0 + 2048;
+    auto weight = [&](int t) { return (long long)(tiles[t].rb - tiles[t].ra) * tiles[t].pad0 + 2048; };
+    auto split = [&](int t0, int t1, std::vector<int>& beg) {        // [t0, t1) into G weight-balanced runs
+      std::vector<long long> pre(t1 - t0 + 1, 0);
+      for (int t = t0; t < t1; ++t) pre[t - t0 + 1] = pre[t - t0] + weight(t);
+      beg.assign(G + 1, t0);
+      for (int b = 1; b < G; ++b)
+        beg[b] = t0 + (int)(std::lower_bound(pre.begin(), pre.end(), pre.back() * b / G) - pre.begin());
+      beg[G] = t1;
+      for (int b = 1; b <= G; ++b) beg[b] = std::max(beg[b], beg[b - 1]);
+    };
     std::vector<int> tbeg(G + 1, 0);
-    for (int b = 1; b < G; ++b)
-      tbeg[b] = (int)(std::lower_bound(pre.begin(), pre.end(), pre[tid] * b / G) - pre.begin());
-    tbeg[G] = tid;
-    for (int b = 1; b <= G; ++b) tbeg[b] = std::max(tbeg[b], tbeg[b - 1]);
+    if (n_btiles < tid && !getenv("QPK_TILE_NO_HSPREAD")) {
+      // Hessian tiles (they write y directly and use no accumulator slots, so
+      // any CTA may run them) are spread over the CTAs: CTA b runs its run of
+      // B tiles, then its run of Hessian tiles -- B work and H work are each
+      // balanced, instead of the last few CTAs running Hessian tiles only
+      std::vector<int> bb, hb;
+      split(0, n_btiles, bb);
+      split(n_btiles, tid, hb);
+      std::vector<TileDescD> re;
+      re.reserve(tiles.size());
+      for (int b = 0; b < G; ++b) {
+        tbeg[b] = (int)re.size();
+        re.insert(re.end(), tiles.begin() + bb[b], tiles.begin() + bb[b + 1]);
+        re.insert(re.end(), tiles.begin() + hb[b], tiles.begin() + hb[b + 1]);
+      }
+      tbeg[G] = (int)re.size();
+      tiles.swap(re);
+    } else {
+      split(0, tid, tbeg);
+    }
     std::vector<int> seen(n, -1), slot_of(n, 0), off(G + 1, 0), ucols, tsl(cols.size(), -1);
     bool ok = true;
     for (int b = 0; b < G && ok; ++b) {
