@@ -3,6 +3,7 @@ ranks (one per GPU) with RANK / WORLD_SIZE / LOCAL_RANK set; under torchrun it
 runs as the rank it is; `--impl reference --gpus N` stays a single process."""
 
 import json
+import re
 import subprocess
 import sys
 from pathlib import Path
@@ -15,7 +16,8 @@ ROOT = Path(__file__).resolve().parents[1]
 def _lines(cmd, env=None):
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=ROOT, env=env)
     assert out.returncode == 0, out.stderr[-2000:]
-    return [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{") and "launch_check" in ln]
+    # (ranks share one stdout: two records may land on one line)
+    return [json.loads(m) for m in re.findall(r"\{[^{}]*\}", out.stdout) if "launch_check" in m]
 
 
 @pytest.mark.timeout(300)
