@@ -34,8 +34,12 @@ def test_gpus_1_runs_in_process():
 
 @pytest.mark.timeout(300)
 def test_under_torchrun_no_second_spawn():
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
     recs = _lines([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                   "--master-addr", "127.0.0.1", "--master-port", "29631", "bench.py", "--gpus", "2",
+                   "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
                    "--launch-check"])
     assert sorted(r["rank"] for r in recs) == [0, 1] and all(r["world"] == 2 for r in recs)
 
