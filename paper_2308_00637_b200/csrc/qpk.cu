@@ -550,11 +550,19 @@ struct HostComm {
   int arrived = 0;
   long long gen = 0;
   std::vector<std::vector<double>> bufs;
-  void barrier() {
+  bool broken = false;
+  // false when a rank never shows up (it failed): the others give up instead of hanging
+  bool barrier() {
     std::unique_lock<std::mutex> lk(mu);
+    if (broken) return false;
     const long long g = gen;
-    if (++arrived == n) { arrived = 0; ++gen; cv.notify_all(); }
-    else cv.wait(lk, [&] { return gen != g; });
+    if (++arrived == n) { arrived = 0; ++gen; cv.notify_all(); return true; }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
   }
 };
 
@@ -1926,11 +1934,13 @@ static int allreduce_sum(qpk_ctx* c, double* buf, size_t count, cudaStream_t s) 
     mine.resize(count);
     CUDA_TRY(cudaMemcpyAsync(mine.data(), buf, count * sizeof(double), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
-    hc->barrier();
+    if (!hc->barrier()) return fail(QPK_E_STATE, "emulated all-reduce: a rank did not arrive");
     std::vector<double> sum(count, 0.0);
-    for (int r = 0; r < hc->n; ++r)
+    for (int r = 0; r < hc->n; ++r) {
+      if (hc->bufs[r].size() != count) return fail(QPK_E_STATE, "emulated all-reduce: ranks disagree on the count");
       for (size_t i = 0; i < count; ++i) sum[i] += hc->bufs[r][i];
-    hc->barrier();                                   // every rank has read all buffers
+    }
+    if (!hc->barrier()) return fail(QPK_E_STATE, "emulated all-reduce: a rank did not arrive");   // all have read
     CUDA_TRY(cudaMemcpyAsync(buf, sum.data(), count * sizeof(double), cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return QPK_OK;
