@@ -18,3 +18,12 @@ def pytest_configure(config):
 @pytest.fixture
 def rng():
     return np.random.default_rng(20240817)
+
+
+def pytest_collection_modifyitems(config, items):
+    """No GPU test may hang the run: a default timeout (pytest-timeout) on every
+    `gpu` test that does not set its own."""
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(900))
+
