@@ -2496,6 +2496,8 @@ int qpk_pcg(qpk_ctx* c, const double* rhs, double tol, int rel, int64_t max_iter
   if (max_iters < 1) return fail(QPK_E_ARG, "max_iters must be at least 1");
   CUDA_TRY(cudaSetDevice(c->device));
   const size_t bytes = c->N() * sizeof(double);
+  // the Jacobi build first: its kernels run while the host stages the (pageable) rhs
+  if (!c->jac_ready) { int rcj = build_jacobi(c); if (rcj) return rcj; }
   CUDA_TRY(cudaMemcpyAsync(c->rhs.p, rhs, bytes, cudaMemcpyHostToDevice, c->stream));
   double* hist_dev = nullptr;
   if (hist) {
