@@ -661,6 +661,7 @@ struct qpk_ctx {
   bool sharded = false;
   void* comm = nullptr;
   HostComm* hostcomm = nullptr;   // test-only host-mediated all-reduce (emulated ranks)
+  bool fold_all = false;          // every rank can run the folded (one all-reduce) slot
   DBuf<double> gscal, lscal2, abuf;
 
   // slot engine
@@ -1692,6 +1693,8 @@ static int build_cluster(qpk_ctx* c) {
 }
 
 // QPK_TIMING=1: host setup phases of qpk_problem_finalize on stderr
+static int allreduce_sum(qpk_ctx* c, double* buf, size_t count, cudaStream_t s);
+
 int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   SetupTimer tm;
   if (!c || !c->building) return fail(QPK_E_STATE, "qpk_problem_finalize: no problem being built");
@@ -1903,6 +1906,23 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
   std::vector<double>().swap(c->h_hv);
   c->building = false;
   c->finalized = true;
+  // Sharded: the ranks must agree on the collectives a slot issues.  The folded
+  // slot (one all-reduce of n + 10 values) needs the tile format with CTA
+  // accumulation on EVERY rank; each rank picks its format from its own shard,
+  // so the choice is settled by one all-reduce here.
+  c->fold_all = false;
+  if (c->sharded) {
+    DBuf<double> flag;
+    CUDA_TRY(flag.alloc(1));
+    const double mine = (c->scatter == QPK_SCATTER_DICT && c->cacc) ? 1.0 : 0.0;
+    CUDA_TRY(cudaMemcpyAsync(flag.p, &mine, sizeof mine, cudaMemcpyHostToDevice, s));
+    int rcf = allreduce_sum(c, flag.p, 1, s);
+    if (rcf) return rcf;
+    double all = 0.0;
+    CUDA_TRY(cudaMemcpyAsync(&all, flag.p, sizeof all, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    c->fold_all = all > c->world - 0.5;
+  }
   tm.lap("finish");
   return QPK_OK;
 }
@@ -2125,7 +2145,7 @@ static bool comb_fused(const qpk_ctx* c) {
 // second all-reduce + decision kernel
 static bool slot_fold(const qpk_ctx* c) {
   const int env = getenv("QPK_SHARD_FOLD") ? atoi(getenv("QPK_SHARD_FOLD")) : 1;
-  return env != 0 && c->sharded && c->scatter == QPK_SCATTER_DICT && c->cacc;
+  return env != 0 && c->sharded && c->fold_all && c->scatter == QPK_SCATTER_DICT && c->cacc;
 }
 
 // does the slot finish B'z with a CSC gather pass (k_slot_csc + seg sums)?
