@@ -1823,6 +1823,7 @@ int qpk_problem_finalize(qpk_ctx* c, int scatter) {
     c->grid_eng = (int)std::max<long long>(1, std::min<long long>((long long)eng_per_sm * c->sms, ework));
     // the partial-sum stride E.G must cover every kernel's blocks (tile CTAs included)
     if (c->scatter == QPK_SCATTER_DICT && c->cacc) c->grid_eng = std::max(c->grid_eng, c->tile_grid);
+    if (c->sharded) c->grid_eng = std::max(c->grid_eng, QPK_FOLD_BLOCKS);   // the folded slot's fixed top geometry
   }
   if (c->scatter == QPK_SCATTER_PANEL) {
     c->panel_grid = std::max(1, std::min(c->sms, c->grid_eng));      // one CTA per SM

@@ -506,6 +506,7 @@ __device__ __forceinline__ void decide(const Engine& E, const Ctrl& c, int par, 
 }
 
 // --------------------------------------------------------------- update ----
+#define QPK_FOLD_BLOCKS 32        // blocks that walk the replicated top block in the folded sharded slot
 #ifndef QPK_UPD_U
 #define QPK_UPD_U 4               // independent double2 pairs in flight per thread
 #endif
@@ -555,6 +556,22 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       return;
     }
     alpha = rz / pap;
+    if (E.fold) {
+      // Folded sharded slot: every rank sums the WHOLE replicated top block
+      // itself and takes the control decision from it, so the sum must come out
+      // bit-identical on all ranks whatever their grids are: the top entries
+      // are walked by a FIXED geometry (QPK_FOLD_BLOCKS blocks), the bottom
+      // entries (whose sums arrive through the all-reduce) by the whole grid.
+      if ((int)blockIdx.x < QPK_FOLD_BLOCKS)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < op.n; i += QPK_FOLD_BLOCKS * blockDim.x) {
+          const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, E.y[i]));
+          E.r[i] = ri;
+          rr += ri * ri;
+          rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
+        }
+      for (int i = op.n + blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+        E.r[i] = __dsub_rn(E.r[i], __dmul_rn(alpha, E.y[i]));
+    } else {
     // scalar head: top entries whose y needs its column partials (CSC / tile
     // modes), rounded up to an even index so the rest runs on double2 pairs
     const int nb = CSC ? min(N, (op.n + 1) & ~1) : 0;
@@ -562,7 +579,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       const double yi = (i < op.n) ? top_value<SC>(E, i) : E.y[i];
       const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, yi));
       E.r[i] = ri;
-      if (E.fold ? i < op.n : owns(op, i)) {
+      if (owns(op, i)) {
         rr += ri * ri;
         rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
       }
@@ -593,7 +610,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
             ri.y = __dsub_rn(ri.y, __dmul_rn(alpha, yv[u].y));
             r2[i] = ri;
             // replicated top entries count once over the ranks (rank 0)
-            const bool cx = E.fold ? 2 * i < op.n : owns(op, 2 * i), cy = E.fold ? 2 * i + 1 < op.n : owns(op, 2 * i + 1);
+            const bool cx = owns(op, 2 * i), cy = owns(op, 2 * i + 1);
             if (cx) { rr += ri.x * ri.x; rzn += ri.x * __dmul_rn(mv[u].x, ri.x); }
             if (cy) { rr += ri.y * ri.y; rzn += ri.y * __dmul_rn(mv[u].y, ri.y); }
           }
@@ -602,12 +619,25 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       if ((N & 1) && N - 1 >= nb && blockIdx.x == 0 && threadIdx.x == 0) {
         const double ri = __dsub_rn(E.r[N - 1], __dmul_rn(alpha, E.y[N - 1]));
         E.r[N - 1] = ri;
-        if (E.fold ? N - 1 < op.n : owns(op, N - 1)) {
+        if (owns(op, N - 1)) {
           rr += ri * ri;
           rzn += ri * __dmul_rn(__ldg(E.minv + N - 1), ri);
         }
       }
     }
+    }
+  } else if (E.fold) {
+    // explicit residual, folded slot: top block by the fixed geometry (see above)
+    const bool store = c.mode == MODE_CHECK;
+    if ((int)blockIdx.x < QPK_FOLD_BLOCKS)
+      for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < op.n; i += QPK_FOLD_BLOCKS * blockDim.x) {
+        const double ri = __dsub_rn(__ldg(E.rhs + i), E.y[i]);
+        if (store) E.r[i] = ri;
+        rr += ri * ri;
+      }
+    if (store)
+      for (int i = op.n + blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+        E.r[i] = __dsub_rn(__ldg(E.rhs + i), E.y[i]);
   } else {
     // explicit residual rhs - K x (CHECK stores it as the new r; FINAL only needs its norm)
     const bool store = c.mode == MODE_CHECK;
@@ -615,7 +645,7 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       const double yi = (CSC && i < op.n) ? top_value<SC>(E, i) : E.y[i];
       const double ri = __dsub_rn(__ldg(E.rhs + i), yi);
       if (store) E.r[i] = ri;
-      if (E.fold ? i < op.n : owns(op, i)) rr += ri * ri;
+      if (owns(op, i)) rr += ri * ri;
     }
   }
   double t = block_sum(rr, red);

@@ -282,6 +282,14 @@ int qpk_multi_pcg(qpk_multi* mm, const double* rhs, double tol, int rel, int64_t
     return e;
   });
   if (rc != QPK_OK) return rc;
+  // every rank takes the control decisions itself: they must have agreed
+  for (size_t r = 1; r < infos.size(); ++r)
+    if (infos[r].iterations != infos[0].iterations || infos[r].status != infos[0].status ||
+        infos[r].converged != infos[0].converged || infos[r].restarts != infos[0].restarts ||
+        infos[r].final_residual_norm != infos[0].final_residual_norm)
+      return fail(QPK_E_STATE, "qpk_multi_pcg: ranks 0 and %d disagree (iterations %d / %d, residual %.17g / %.17g)",
+                  (int)r, infos[0].iterations, infos[r].iterations, infos[0].final_residual_norm,
+                  infos[r].final_residual_norm);
   if (info) {
     *info = infos[0];
     for (const auto& o : infos) info->kernel_ms = std::max(info->kernel_ms, o.kernel_ms);   // max over devices
