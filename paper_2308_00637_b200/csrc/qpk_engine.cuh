@@ -506,7 +506,7 @@ __device__ __forceinline__ void decide(const Engine& E, const Ctrl& c, int par, 
 }
 
 // --------------------------------------------------------------- update ----
-#define QPK_FOLD_BLOCKS 32        // blocks that walk the replicated top block in the folded sharded slot
+#define QPK_FOLD_BLOCKS 128       // blocks that walk the replicated top block in the folded sharded slot
 #ifndef QPK_UPD_U
 #define QPK_UPD_U 4               // independent double2 pairs in flight per thread
 #endif
@@ -562,15 +562,54 @@ __global__ void __launch_bounds__(QPK_BLOCK) k_slot_update(Engine E, int par) {
       // bit-identical on all ranks whatever their grids are: the top entries
       // are walked by a FIXED geometry (QPK_FOLD_BLOCKS blocks), the bottom
       // entries (whose sums arrive through the all-reduce) by the whole grid.
-      if ((int)blockIdx.x < QPK_FOLD_BLOCKS)
-        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < op.n; i += QPK_FOLD_BLOCKS * blockDim.x) {
+      if ((int)blockIdx.x < QPK_FOLD_BLOCKS) {
+        // pairs (16-byte accesses; r, y, minv are 16-byte aligned), the odd last entry by one thread
+        const int ntp = op.n >> 1, stride = QPK_FOLD_BLOCKS * blockDim.x;
+        double2* r2 = reinterpret_cast<double2*>(E.r);
+        const double2* y2 = reinterpret_cast<const double2*>(E.y);
+        const double2* m2 = reinterpret_cast<const double2*>(E.minv);
+        for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < ntp; base += 2 * stride) {
+          const int i1 = base + stride;
+          double2 ra = r2[base], ya = y2[base], ma = __ldg(m2 + base), rb, yb, mb;
+          if (i1 < ntp) { rb = r2[i1]; yb = y2[i1]; mb = __ldg(m2 + i1); }
+          ra.x = __dsub_rn(ra.x, __dmul_rn(alpha, ya.x));
+          ra.y = __dsub_rn(ra.y, __dmul_rn(alpha, ya.y));
+          r2[base] = ra;
+          rr += ra.x * ra.x; rzn += ra.x * __dmul_rn(ma.x, ra.x);
+          rr += ra.y * ra.y; rzn += ra.y * __dmul_rn(ma.y, ra.y);
+          if (i1 < ntp) {
+            rb.x = __dsub_rn(rb.x, __dmul_rn(alpha, yb.x));
+            rb.y = __dsub_rn(rb.y, __dmul_rn(alpha, yb.y));
+            r2[i1] = rb;
+            rr += rb.x * rb.x; rzn += rb.x * __dmul_rn(mb.x, rb.x);
+            rr += rb.y * rb.y; rzn += rb.y * __dmul_rn(mb.y, rb.y);
+          }
+        }
+        if ((op.n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+          const int i = op.n - 1;
           const double ri = __dsub_rn(E.r[i], __dmul_rn(alpha, E.y[i]));
           E.r[i] = ri;
           rr += ri * ri;
           rzn += ri * __dmul_rn(__ldg(E.minv + i), ri);
         }
-      for (int i = op.n + blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
-        E.r[i] = __dsub_rn(E.r[i], __dmul_rn(alpha, E.y[i]));
+      }
+      {
+        constexpr int U = 4;
+        const int stride = gridDim.x * blockDim.x;
+        for (int base = op.n + blockIdx.x * blockDim.x + threadIdx.x; base < N; base += U * stride) {
+          double rv[U], yv[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = base + u * stride;
+            if (i < N) { rv[u] = E.r[i]; yv[u] = E.y[i]; }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int i = base + u * stride;
+            if (i < N) E.r[i] = __dsub_rn(rv[u], __dmul_rn(alpha, yv[u]));
+          }
+        }
+      }
     } else {
     // scalar head: top entries whose y needs its column partials (CSC / tile
     // modes), rounded up to an even index so the rest runs on double2 pairs
